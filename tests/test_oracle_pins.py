@@ -1,0 +1,321 @@
+"""Pins of the float64 oracle against what the paper and mathematics fix (no GPU).
+
+Each test names the PAPER.md passage (P:n) or the independent fact it checks.  None of them retypes the
+oracle's own formula: they use closed forms, paper numbers (tests/golden/), textbook routines (numpy.fft),
+independent algebraic identities, brute force, and physics-level injections through workloads/scenes.py.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import srpphat as srp
+from oracle import svdphat as svd
+from oracle.kdtree import KDTree
+from workloads import geometry as G
+from workloads import scenes as S
+
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _gold(name):
+    with open(os.path.join(GOLD, name)) as f:
+        return json.load(f)
+
+
+def _paper_mics(name):
+    return np.asarray(_gold("paper_table2_cm.json")[name], dtype=np.float64) / 100.0
+
+
+T1 = _gold("paper_table1.json")
+FS, C = float(T1["fs"]), float(T1["c"])
+
+
+# ------------------------------------------------------------------ eq. 1 / eq. 2
+def test_tdoa_farfield_closed_form():
+    mics = _paper_mics("1d")
+    tau = srp.tdoa_farfield(mics, np.array([[0.0, 0.0, 1.0], [1.0, 0.0, 0.0], [0.0, 0.0, -1.0]]), FS, C)
+    p = srp.pairs(7).index((0, 6))
+    assert tau[0, p] == pytest.approx(16000.0 / 343.0 * 0.10, abs=1e-12)   # 4.664723 samples
+    assert tau[1, p] == pytest.approx(0.0, abs=1e-15)                      # orthogonal to the baseline
+    assert np.allclose(tau[2], -tau[0], atol=0)                            # antisymmetric in u
+    # non-unit s_q is normalised by eq. 2 itself
+    tau2 = srp.tdoa_farfield(mics, np.array([[0.0, 0.0, 7.5]]), FS, C)
+    assert np.allclose(tau2[0], tau[0], atol=1e-13)
+
+
+def test_tdoa_bound_and_pair_antisymmetry():
+    rng = np.random.default_rng(0)
+    mics = rng.uniform(-0.1, 0.1, (6, 3))
+    u = rng.standard_normal((200, 3))
+    for fld, pts in (("far", u), ("near", u * 0.7)):
+        tau = srp.tdoa(mics, pts, FS, C, fld)
+        for p, (i, j) in enumerate(srp.pairs(6)):
+            lim = FS / C * np.linalg.norm(mics[i] - mics[j])
+            assert np.all(np.abs(tau[:, p]) <= lim * (1 + 1e-12))
+        # swapping the mic order of the array reverses each pair's sign
+        tau_sw = srp.tdoa(mics[::-1], pts, FS, C, fld)
+        P = len(srp.pairs(6))
+        for p, (i, j) in enumerate(srp.pairs(6)):
+            q = srp.pairs(6).index((5 - j, 5 - i))
+            assert np.allclose(tau_sw[:, q], -tau[:, p], atol=1e-12)
+        assert P == 15
+
+
+def test_tdoa_exact_closed_form_and_farfield_limit():
+    mics = _paper_mics("1d")
+    p = srp.pairs(7).index((0, 6))
+    tau = srp.tdoa_exact(mics, np.array([[0.0, 0.0, 1.0], [1.0, 0.0, 0.0]]), FS, C)
+    assert tau[0, p] == pytest.approx(16000.0 / 343.0 * (1.05 - 0.95), abs=1e-12)
+    assert tau[1, p] == pytest.approx(0.0, abs=1e-12)
+    # far-field convergence: at R = 100 * aperture, |tau_exact - tau_far| < 0.01 samples
+    rng = np.random.default_rng(1)
+    u = rng.standard_normal((100, 3))
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    R = 100 * 0.10
+    d = srp.tdoa_exact(mics, R * u, FS, C) - srp.tdoa_farfield(mics, u, FS, C)
+    assert np.max(np.abs(d)) < 0.01
+
+
+# ------------------------------------------------------------------ STFT
+def test_stft_equals_numpy_rfft():
+    rng = np.random.default_rng(2)
+    fr = rng.standard_normal((3, 4, 64))
+    X = srp.stft(fr)
+    ref = np.fft.rfft(fr * np.sin(np.pi * (np.arange(64) + 0.5) / 64), axis=-1)
+    assert np.max(np.abs(X - ref)) < 1e-11 * np.max(np.abs(ref))
+
+
+def test_stft_tone_and_dc():
+    N = 512
+    n = np.arange(N)
+    X = srp.stft(np.cos(2 * np.pi * 16 * n / N)[None, None, :])[0, 0]
+    assert int(np.argmax(np.abs(X))) == 16
+    Xdc = np.abs(srp.stft(np.ones((1, 1, N)))[0, 0])
+    assert set(np.argsort(Xdc)[-2:]) == {0, 1}          # sine-window main lobe
+
+
+def test_framing_counts():
+    assert srp.frame_count(32000, 512, 256) == 124      # BJ.cfg1 "~124 frames"
+    assert srp.frame_count(960000, 512, 256) == 3749    # BJ.cfg2 "~3750 frames"
+    assert srp.frame_count(511, 512, 256) == 0
+    assert srp.frame_count(512, 512, 256) == 1
+    a = np.arange(2 * 1000, dtype=np.float32).reshape(2, 1000)
+    fr = srp.extract_frames(a, srp.frame_count(1000, 64, 32), 2, 64, 1000, 32)
+    assert fr.shape == (30, 2, 64)
+    assert fr[7, 1, 5] == 1000 + 7 * 32 + 5
+
+
+# ------------------------------------------------------------------ eq. 3 / eq. 7
+def test_cross_spectrum_conventions():
+    rng = np.random.default_rng(3)
+    K, N = 33, 64
+    Xi = rng.standard_normal(K) + 1j * rng.standard_normal(K)
+    k = np.arange(K)
+    d = 3
+    X = np.stack([Xi, 2.5 * Xi * np.exp(-2j * np.pi * k * d / N), Xi, np.zeros(K)])[None]
+    x = srp.cross_spectrum(X).reshape(6, K)
+    P = srp.pairs(4)
+    assert np.allclose(x[P.index((0, 2))], 1.0, atol=1e-15)                          # identical channels
+    assert np.allclose(x[P.index((0, 1))], np.exp(2j * np.pi * k * d / N), atol=1e-14)  # +2 pi k d / N
+    assert np.all(x[P.index((0, 3))] == 0) and np.all(x[P.index((2, 3))] == 0)        # zero guard
+    assert np.allclose(np.abs(x[[P.index((0, 1)), P.index((0, 2)), P.index((1, 2))]]), 1.0, atol=1e-14)
+    # pair-major with bins inner (eq. 7)
+    xf = srp.cross_spectrum(X)[0]
+    assert xf[P.index((0, 1)) * K + 5] == x[P.index((0, 1)), 5]
+
+
+# ------------------------------------------------------------------ W, Y (eqs. 4, 5, 8, 9)
+def _small_case(level=2, N=64, name="3d"):
+    mics = _paper_mics(name)
+    grid = G.icosphere(level)
+    return mics, grid, srp.tdoa_farfield(mics, grid, FS, C), N
+
+
+def test_steering_frobenius_and_self_match():
+    mics, grid, tau, N = _small_case(4, 256, "3d")
+    K = N // 2 + 1
+    Q, P = tau.shape
+    tot = 0.0
+    for q0 in range(0, Q, 512):
+        W = srp.steering_rows(tau[q0:q0 + 512], N)
+        tot += np.sum(np.abs(W) ** 2)
+    assert tot == pytest.approx(Q * P * K, rel=1e-12)        # 2562*21*129 = 6,940,458 (|W| = 1)
+    assert Q * P * K == 6940458
+    assert srp.steering_rows(tau[:1], N)[0, :K].real[0] == 1.0   # k = 0 column is 1
+    qs = np.array([5, 777, 2000])
+    x = np.conj(srp.steering_rows(tau[qs], N))
+    Y = srp.srp_energy(tau, x, N)
+    for r, q in enumerate(qs):
+        assert Y[r, q] == pytest.approx(P * K, rel=1e-12)
+        assert np.all(Y[r] <= P * K * (1 + 1e-12))
+    qb, _ = srp.argmax_tie(Y)
+    assert list(qb) == list(qs)
+
+
+def test_srp_energy_equals_literal_eq5():
+    rng = np.random.default_rng(4)
+    mics, grid, tau, N = _small_case(1, 32)
+    X = rng.standard_normal((2, 7, N // 2 + 1)) + 1j * rng.standard_normal((2, 7, N // 2 + 1))
+    X[1, 3, 4] = 0.0
+    x = srp.cross_spectrum(X)
+    Y = srp.srp_energy(tau, x, N)
+    for f in range(2):
+        for q in (0, 17, 41):
+            assert Y[f, q] == pytest.approx(srp.srp_energy_direct(tau[q], X[f], N), rel=1e-11, abs=1e-10)
+
+
+def test_srp_energy_delay_and_sum_identity():
+    """Independent O(QMK) formula: tau_qij = d_qi - d_qj gives
+    Y_q = 1/2 sum_k (|sum_m e_m[k] exp(+j2pi k d_qm / N)|^2 - n_k), n_k = #non-zero phasors at bin k."""
+    rng = np.random.default_rng(5)
+    mics, grid, tau, N = _small_case(2, 64)
+    K = N // 2 + 1
+    fr = rng.standard_normal((3, 7, N))
+    fr[2, 4] = 0.0                                           # one silent channel
+    X = srp.stft(fr)
+    x = srp.cross_spectrum(X)
+    Y = srp.srp_energy(tau, x, N)
+    delay = -(FS / C) * grid @ mics.T                        # (Q, M) arrival delays, any common offset
+    e = np.where(np.abs(X) > 0, X / np.where(np.abs(X) > 0, np.abs(X), 1), 0)
+    k = np.arange(K)
+    for f in range(3):
+        nk = np.sum(np.abs(e[f]) > 0, axis=0)
+        a = e[f][None, :, :] * np.exp(2j * np.pi * k[None, None, :] * delay[:, :, None] / N)   # (Q, M, K)
+        ds = 0.5 * np.sum(np.abs(a.sum(axis=1)) ** 2 - nk[None, :], axis=1)
+        assert np.max(np.abs(ds - Y[f])) < 1e-9 * np.max(np.abs(Y[f]))
+
+
+def test_injection_returns_grid_point_3d():
+    """Noiseless fractional-delay plane waves from grid directions (workloads.scenes physics) -> q (sign pin)."""
+    mics, grid, tau, N = _small_case(3, 256, "3d")
+    rng = np.random.default_rng(6)
+    qs = rng.choice(grid.shape[0], 12, replace=False)
+    fr = np.stack([S.plane_wave_stream(rng, mics, FS, C, N, grid[q], 300.0) for q in qs])
+    x = srp.frames_to_x(fr)
+    qb, _ = srp.srp_localize(tau, x, N)
+    assert list(qb) == list(qs)
+    # flipping the sign of eq. 4 would point at the antipode
+    Yflip = srp.srp_energy(-tau, x, N)
+    anti = np.argmin(grid @ grid[qs].T, axis=0)
+    assert list(np.argmax(Yflip, axis=1)) == list(anti)
+
+
+def test_injection_planar_twin_lowest_index():
+    mics, grid, tau, N = _small_case(3, 256, "2d")
+    rng = np.random.default_rng(7)
+    mirror = {i: int(np.argmin(np.linalg.norm(grid - grid[i] * [1, 1, -1], axis=1))) for i in range(len(grid))}
+    qs = [q for q in rng.choice(grid.shape[0], 40, replace=False) if mirror[q] != q][:8]
+    fr = np.stack([S.plane_wave_stream(rng, mics, FS, C, N, grid[q], 300.0) for q in qs])
+    qb, _ = srp.srp_localize(tau, srp.frames_to_x(fr), N)
+    assert list(qb) == [min(q, mirror[q]) for q in qs]
+
+
+def test_degenerate_frame():
+    mics, grid, tau, N = _small_case(1, 32)
+    fr = np.zeros((2, 7, N))
+    fr[1, 0] = np.random.default_rng(8).standard_normal(N)     # only one live channel: X vector is 0
+    q, s = srp.srp_localize(tau, srp.frames_to_x(fr), N)
+    assert list(q) == [-1, -1] and list(s) == [0.0, 0.0]
+
+
+# ------------------------------------------------------------------ rank rule (eq. 11) vs the paper's gains
+@pytest.mark.parametrize("name", ["1d", "2d", "3d"])
+def test_rank_rule_reproduces_paper_gains(name):
+    gains = _gold("paper_gains.json")
+    mics = _paper_mics(name)
+    grid = G.icosphere(4)
+    assert grid.shape[0] == T1["Q"]
+    tau = srp.tdoa_farfield(mics, grid, FS, C)
+    fac = svd.svd_factors(tau, T1["N"], gains["delta"], method="svd")
+    assert fac["total"] == pytest.approx(grid.shape[0] * 21 * (T1["N"] // 2 + 1), rel=1e-12)
+    assert round(T1["Q"] / fac["D"]) == gains["gain"][name]
+    # minimality: D-1 violates eq. 11
+    s2 = fac["sigma2"]
+    assert np.sum(s2[:fac["D"]]) >= (1 - gains["delta"]) * fac["total"]
+    assert np.sum(s2[:fac["D"] - 1]) < (1 - gains["delta"]) * fac["total"]
+
+
+def test_rank_one_toy():
+    tau = np.zeros((5, 1))                      # identical rows
+    fac = svd.svd_factors(tau, 2, 1e-3, method="svd")
+    assert fac["D"] == 1
+
+
+def test_svd_and_gram_routes_agree():
+    mics, grid, tau, N = _small_case(2, 64, "2d")
+    a = svd.svd_factors(tau, N, 1e-5, method="svd")
+    b = svd.svd_factors(tau, N, 1e-5, method="gram", chunk=100)
+    assert a["D"] == b["D"]
+    n = min(len(a["sigma2"]), 40)
+    assert np.allclose(a["sigma2"][:n], b["sigma2"][:n], rtol=1e-9, atol=1e-9 * a["sigma2"][0])
+    rng = np.random.default_rng(9)
+    x = srp.frames_to_x(rng.standard_normal((4, 7, N)))
+    for f in (a, b):
+        f["_s"] = svd.search_scores(f["Rhat"], svd.project(f["V"], x) /
+                                    np.linalg.norm(svd.project(f["V"], x), axis=1, keepdims=True))
+    assert np.max(np.abs(a["_s"] - b["_s"])) < 1e-9
+
+
+def test_full_rank_svd_equals_srp():
+    mics, grid, tau, N = _small_case(2, 64, "3d")
+    rng = np.random.default_rng(10)
+    fac = svd.svd_factors(tau, N, 1e-14, method="svd")
+    u = rng.standard_normal((30, 3))
+    fr = np.stack([S.plane_wave_stream(rng, mics, FS, C, N, uu / np.linalg.norm(uu), 5.0) for uu in u])
+    x = srp.frames_to_x(fr)
+    q1, s1 = srp.srp_localize(tau, x, N)
+    q2, s2 = svd.svd_localize(fac, tau, x, N)
+    assert list(q1) == list(q2)
+    assert np.allclose(s1, s2, rtol=1e-10)
+
+
+def test_eq15_distance_identity():
+    rng = np.random.default_rng(11)
+    a = rng.standard_normal((1000, 9)) + 1j * rng.standard_normal((1000, 9))
+    b = rng.standard_normal((1000, 9)) + 1j * rng.standard_normal((1000, 9))
+    a /= np.linalg.norm(a, axis=1, keepdims=True)
+    b /= np.linalg.norm(b, axis=1, keepdims=True)
+    lhs = np.real(np.sum(a * b, axis=1))
+    rhs = 1 - 0.5 * np.sum(np.abs(a - np.conj(b)) ** 2, axis=1)
+    assert np.max(np.abs(lhs - rhs)) < 1e-12
+
+
+def test_svd_injection_returns_grid_point():
+    mics, grid, tau, N = _small_case(3, 256, "3d")
+    fac = svd.svd_factors(tau, N, 1e-5, method="svd")
+    rng = np.random.default_rng(12)
+    qs = rng.choice(grid.shape[0], 10, replace=False)
+    fr = np.stack([S.plane_wave_stream(rng, mics, FS, C, N, grid[q], 300.0) for q in qs])
+    x = srp.frames_to_x(fr)
+    q, s = svd.svd_localize(fac, tau, x, N)
+    assert list(q) == list(qs)
+    qt, _ = svd.svd_localize(fac, tau, x, N, use_tree=True)
+    assert list(qt) == list(qs)
+
+
+# ------------------------------------------------------------------ k-d tree == brute force
+@pytest.mark.parametrize("n,dim", [(12, 2), (42, 4), (162, 16), (300, 3)])
+def test_kdtree_equals_brute_force(n, dim):
+    rng = np.random.default_rng(n + dim)
+    pts = rng.standard_normal((n, dim))
+    pts[n // 2] = pts[3]                              # exact duplicates / twins
+    pts[n - 1] = pts[0]
+    pts = np.round(pts, 2)                            # many exact distance ties
+    t = KDTree(pts, leaf_size=4)
+    for _ in range(200):
+        qv = np.round(rng.standard_normal(dim), 1) if _ % 2 else pts[rng.integers(n)]
+        d = np.array([float((p - qv) @ (p - qv)) for p in pts])   # same per-point arithmetic as the tree
+        brute = int(np.argmin(d))                     # numpy argmin returns the lowest index on ties
+        i, d2 = t.nearest(qv)
+        assert i == brute and d2 == d[brute]
+
+
+def test_kdtree_singleton_and_self_query():
+    t = KDTree(np.array([[1.0, 2.0]]))
+    assert t.nearest(np.array([5.0, -3.0]))[0] == 0
+    pts = np.random.default_rng(13).standard_normal((100, 6))
+    t = KDTree(pts)
+    for i in range(100):
+        assert t.nearest(pts[i]) == (i, 0.0)
