@@ -1,0 +1,140 @@
+/*
+ * svdphat.h — C-ABI of libsvdphat.so, the B200 (sm_100a) per-frame localisation hot path of
+ * SVD-PHAT and of the exact SRP-PHAT it approximates (Grondin & Glass, arXiv 1811.11785).
+ *
+ * Citations: PAPER.md = /root/reference/PAPER.md (line numbers, section / equation / algorithm).
+ * Readings of silent or ambiguous passages are the R* items of DESIGN.md.
+ *
+ * Boundary: plain pointers and sizes only, no torch types.  A plan is created once
+ * (Alg. 1 "Offline") and then localises batches of frames (Alg. 1 "Online",
+ * PAPER.md:191-197; SRP-PHAT eqs. 5-6).
+ *
+ * Error behaviour: every call returns an svdphat_status and never throws across the ABI.  All arguments are
+ * validated before any kernel is launched; on a non-OK status no output is written and
+ * svdphat_last_error() returns a thread-local human-readable detail.  Asynchronous device faults surface at
+ * the caller's next synchronisation of the stream.
+ */
+#ifndef SVDPHAT_H_
+#define SVDPHAT_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+    SVDPHAT_OK = 0,
+    SVDPHAT_INVALID_ARG = 1,   /* argument violates a documented precondition                          */
+    SVDPHAT_ALLOC = 2,         /* device or host allocation failed                                      */
+    SVDPHAT_CUDA = 3,          /* a CUDA runtime / driver / cuBLAS / cuSOLVER call failed               */
+    SVDPHAT_NUMERIC = 4,       /* setup produced non-finite values (e.g. eigensolver failure)           */
+    SVDPHAT_UNSUPPORTED = 5,   /* valid but not supported by this build (e.g. no sm_100a device)        */
+    SVDPHAT_TOO_LARGE = 6      /* the plan would not fit the device memory or index ranges              */
+} svdphat_status;
+
+enum { SVDPHAT_FIELD_FAR = 0, SVDPHAT_FIELD_NEAR = 1 };
+enum { SVDPHAT_METHOD_SRP = 1, SVDPHAT_METHOD_SVD = 2 };
+
+typedef struct svdphat_plan_s* svdphat_plan_t;
+
+/* Plan description.  All pointers are HOST pointers, read only during svdphat_plan_create (not retained). */
+typedef struct {
+    int32_t M;                 /* microphones, 2..32 ("array with M microphones")                */
+    const double* mic_xyz;     /* M x 3 row-major, metres, finite (r_i)                          */
+    double fs;                 /* sample rate f_S > 0, Hz                                        */
+    double c;                  /* speed of sound c > 0, m/s                                      */
+    int32_t N;                 /* frame size, power of two in [16, 2048]                         */
+    int32_t hop;               /* hop Delta N, 0 < hop <= N; informational for streams            */
+    int32_t field;             /* SVDPHAT_FIELD_FAR: eq. 2 on directions s_q (normalised here);
+                                  SVDPHAT_FIELD_NEAR: eq. 1 on points s_q in metres             */
+    int32_t Q;                 /* candidates, 1..2^24                                             */
+    const double* points_xyz;  /* Q x 3 row-major; FAR: any non-zero finite vector; NEAR: finite position      */
+    int32_t rank_D;            /* SVD rank: > 0 explicit, 0 = rule of eq. 11 with delta          */
+    double delta;              /* eq. 11 tolerance, 0 < delta < 1 (BASELINE cfg1: 1e-5)                         */
+    int32_t methods;           /* bitmask of SVDPHAT_METHOD_SRP | SVDPHAT_METHOD_SVD                           */
+    int64_t max_frames;        /* largest n_frames of a single localize call (sizes the device workspace)       */
+    int32_t device;            /* CUDA device ordinal                                                          */
+} svdphat_plan_desc;
+
+typedef struct {
+    int32_t M, P, N, K_bins;   /* P = M(M-1)/2 pairs, K_bins = N/2+1                             */
+    int64_t PK;                /* length of the X vector, P*(N/2+1) (eq. 7)                        */
+    int32_t Q;                 /* candidates                                                                    */
+    int32_t Q_classes;         /* distinct steering rows of W (bitwise-identical rows merged; R11)    */
+    int32_t D;                 /* retained SVD rank (paper's K, eq. 11), 0 if SVD not planned                   */
+    double energy_kept;        /* sum_{d<=D} sigma_d^2 / Tr{W W^H}                                              */
+    double trace_WWH;          /* Tr{W W^H} = Q*P*(N/2+1) exactly (|W| = 1)                                     */
+    int32_t methods;
+    int32_t gemm_k;            /* padded contraction length of the device real-split GEMMs                      */
+    int64_t max_frames;
+    int64_t bytes_W;           /* device bytes of the FP16 real-split steering matrix (SRP)                     */
+    int64_t bytes_V;           /* device bytes of the FP16 real-split V_D (SVD)                                 */
+    int64_t bytes_R;           /* device bytes of the split-FP16 normalised dictionary rows (SVD)               */
+    int64_t bytes_workspace;   /* per-call workspace (phasors, keys, Z, ...)                                    */
+    double setup_seconds;      /* wall time of svdphat_plan_create                                              */
+} svdphat_plan_info_t;
+
+/* Alg. 1 offline steps 1-3: TDOAs (eq. 1/2), W (eqs. 4, 8), SVD (eq. 10) with the rank rule
+ * (eq. 11), dictionary rows D = US (eq. 13) normalised.  Float64 setup, run once; the k-d tree of
+ * step 4 is replaced by an exhaustive contraction.  *out receives an opaque plan owned by the caller
+ * (free with svdphat_plan_destroy).  Returns INVALID_ARG for bad descriptors (M<2 or >32, N not a power of two,
+ * hop<=0 or >N, fs<=0, c<=0, non-finite coordinates, zero FAR direction, delta outside (0,1), methods==0,
+ * max_frames<0), UNSUPPORTED if the device is not sm_100, ALLOC/TOO_LARGE if memory is insufficient. */
+svdphat_status svdphat_plan_create(const svdphat_plan_desc* desc, svdphat_plan_t* out);
+
+/* Fills *out (host struct).  INVALID_ARG on NULL. */
+svdphat_status svdphat_plan_info(svdphat_plan_t plan, svdphat_plan_info_t* out);
+
+/* Copies the first min(n, Q_classes) squared singular values sigma_d^2 of W, descending (host array), so that a
+ * caller can re-apply eq. 11 for any delta (Fig. 2b/2c).  INVALID_ARG if SVD was not planned. */
+svdphat_status svdphat_plan_sigma2(svdphat_plan_t plan, double* out, int32_t n);
+
+/* Localise n_frames frames on `stream` (a cudaStream_t, NULL = legacy default stream); asynchronous, no host
+ * synchronisation and no allocation (graph-capturable).
+ *   method   SVDPHAT_METHOD_SRP: eqs. 5-6 = Y = Re{W X} (eq. 9) + argmax;
+ *            SVDPHAT_METHOD_SVD: Alg. 1 online: Z = V^H X (eq. 12), nearest normalised
+ *            dictionary row (eqs. 14-15), then Y_q from the row of W.
+ *   d_audio  DEVICE float32 samples: sample n of channel m in frame l is d_audio[m*channel_stride +
+ *            l*frame_stride + n] (stream [M][L]: channel_stride=L, frame_stride=hop; framed [B][M][N]:
+ *            channel_stride=N, frame_stride=M*N).  Must be 4-byte aligned.
+ *   d_doa    DEVICE int32[n_frames]: 0-based index into the plan's points; lowest index among exact ties
+ *            (R10); -1 when the frame's X vector is identically 0 (R4).
+ *   d_score  DEVICE float32[n_frames]: Y_q_bar (eq. 5 at q_bar), 0 when d_doa = -1.
+ * Buffers are owned by the caller.  0 <= n_frames <= max_frames.  One localize in flight per plan (the plan's
+ * workspace is shared).  INVALID_ARG on violated preconditions, CUDA on launch failure. */
+svdphat_status svdphat_localize(svdphat_plan_t plan, int32_t method, const float* d_audio, int64_t n_frames,
+                                int64_t channel_stride, int64_t frame_stride, int32_t* d_doa, float* d_score,
+                                void* stream);
+
+/* Same with HOST buffers: copies audio elements [0, audio_elems) host->device, localises, copies results back
+ * and synchronises `stream`.  h_audio should be pinned for full bandwidth.  The device staging buffer is
+ * allocated on first use and kept by the plan (ALLOC on failure). */
+svdphat_status svdphat_localize_host(svdphat_plan_t plan, int32_t method, const float* h_audio,
+                                     int64_t audio_elems, int64_t n_frames, int64_t channel_stride,
+                                     int64_t frame_stride, int32_t* h_doa, float* h_score, void* stream);
+
+/* Releases all device and host memory of the plan (NULL is a no-op).  The caller must have synchronised any
+ * stream a localize was issued on. */
+void svdphat_plan_destroy(svdphat_plan_t plan);
+
+/* Number of frames of an L-sample stream without padding: 1 + floor((L - N)/hop), 0 if L < N (R3). */
+int64_t svdphat_frame_count(int64_t L, int32_t N, int32_t hop);
+
+const char* svdphat_status_str(svdphat_status s);
+const char* svdphat_last_error(void);
+
+/* ---- test-only introspection (not part of the product path; used by tests/ for kernel-unit parity) ---- */
+enum {
+    SVDPHAT_DUMP_PHASORS = 1,  /* FP16 unit phasors of the last call, decoded to float32 [F][M][K_bins][2]     */
+    SVDPHAT_DUMP_Z = 2,        /* float32 Z of the last SVD call [F][2*D] (Re then Im), scaled by sqrt(PK)       */
+    SVDPHAT_DUMP_CLASS_REP = 3,/* int32 [Q_classes]: representative (lowest) point index of each steering class */
+    SVDPHAT_DUMP_KEYS = 4      /* uint64 [F]: packed (score, class) argmax keys of the last call                 */
+};
+svdphat_status svdphat_debug_dump(svdphat_plan_t plan, int32_t what, int64_t n_frames, void* host_out,
+                                  int64_t bytes);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SVDPHAT_H_ */

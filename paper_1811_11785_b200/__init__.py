@@ -1,0 +1,7 @@
+"""B200-native SVD-PHAT / SRP-PHAT per-frame localisation (arXiv 1811.11785).
+
+The product is libsvdphat.so (C-ABI in include/svdphat.h, CUDA kernels for sm_100a in csrc/); this package is its
+thin Python binding.  Importing it loads the shared library and fails loudly if it is missing.
+"""
+from ._lib import (DUMP_CLASS_REP, DUMP_KEYS, DUMP_PHASORS, DUMP_Z, LIB_PATH, Plan, SvdPhatError,  # noqa: F401
+                   frame_count, lib)

@@ -1,0 +1,467 @@
+// api.cu — the C-ABI of libsvdphat (include/svdphat.h): validation, float64 geometry, steering classes, plan
+// assembly and the per-call orchestration of the hot path kernels.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "internal.h"
+
+namespace svdphat {
+
+static thread_local std::string g_err;
+void set_error(const std::string& msg) { g_err = msg; }
+
+static svdphat_status fail(svdphat_status s, const std::string& msg) {
+    g_err = msg;
+    return s;
+}
+
+// ---------------------------------------------------------------- TMA descriptor encoding (driver entry point)
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* ptr = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(ptr);
+    }
+    return fn;
+}
+
+// 2-D FP16 row-major [rows][cols] tensor, box = 64 cols (128 B) x box_rows, 128-byte swizzle
+static bool encode_2d(CUtensorMap* tm, const void* base, int64_t rows, int64_t cols, int box_rows) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
+static Layout make_layout(int M, int N) {
+    Layout L;
+    L.M = M;
+    L.Mi = M <= 4 ? 4 : M <= 8 ? 8 : M <= 16 ? 16 : 32;
+    L.P = M * (M - 1) / 2;
+    L.Pi = L.Mi * (L.Mi - 1) / 2;
+    L.N = N;
+    L.Kb = N / 2 + 1;
+    L.bpc = L.Mi <= 16 ? 4 : 2;
+    L.n_chunks = (L.Kb + L.bpc - 1) / L.bpc;
+    const int units = L.bpc == 4 ? L.Pi : (L.Pi + 1) / 2;
+    L.U = (units + 7) / 8 * 8;
+    L.K_total = (int64_t)L.n_chunks * L.U * 8;
+    L.unit_bytes = L.bpc * 4;
+    return L;
+}
+
+static svdphat_status validate(const svdphat_plan_desc* d) {
+    if (!d) return fail(SVDPHAT_INVALID_ARG, "desc is NULL");
+    if (d->M < 2 || d->M > 32) return fail(SVDPHAT_INVALID_ARG, "M must be in [2, 32]");
+    if (!d->mic_xyz || !d->points_xyz) return fail(SVDPHAT_INVALID_ARG, "mic_xyz / points_xyz is NULL");
+    if (!(d->fs > 0) || !std::isfinite(d->fs)) return fail(SVDPHAT_INVALID_ARG, "fs must be > 0");
+    if (!(d->c > 0) || !std::isfinite(d->c)) return fail(SVDPHAT_INVALID_ARG, "c must be > 0");
+    if (d->N < 16 || d->N > 2048 || (d->N & (d->N - 1)))
+        return fail(SVDPHAT_INVALID_ARG, "N must be a power of two in [16, 2048]");
+    if (d->hop <= 0 || d->hop > d->N) return fail(SVDPHAT_INVALID_ARG, "hop must be in (0, N]");
+    if (d->field != SVDPHAT_FIELD_FAR && d->field != SVDPHAT_FIELD_NEAR)
+        return fail(SVDPHAT_INVALID_ARG, "field must be FAR or NEAR");
+    if (d->Q < 1 || d->Q > (1 << 24)) return fail(SVDPHAT_INVALID_ARG, "Q must be in [1, 2^24]");
+    if (d->methods <= 0 || (d->methods & ~(SVDPHAT_METHOD_SRP | SVDPHAT_METHOD_SVD)))
+        return fail(SVDPHAT_INVALID_ARG, "methods must be a non-empty subset of SRP|SVD");
+    if ((d->methods & SVDPHAT_METHOD_SVD) && d->rank_D <= 0 && !(d->delta > 0 && d->delta < 1))
+        return fail(SVDPHAT_INVALID_ARG, "delta must be in (0, 1)");
+    if (d->rank_D < 0) return fail(SVDPHAT_INVALID_ARG, "rank_D must be >= 0");
+    if (d->max_frames < 0 || d->max_frames > (1ll << 26)) return fail(SVDPHAT_INVALID_ARG, "max_frames out of range");
+    for (int i = 0; i < 3 * d->M; ++i)
+        if (!std::isfinite(d->mic_xyz[i])) return fail(SVDPHAT_INVALID_ARG, "non-finite microphone coordinate");
+    for (int64_t q = 0; q < d->Q; ++q) {
+        const double* s = d->points_xyz + 3 * q;
+        if (!std::isfinite(s[0]) || !std::isfinite(s[1]) || !std::isfinite(s[2]))
+            return fail(SVDPHAT_INVALID_ARG, "non-finite candidate point " + std::to_string(q));
+        if (d->field == SVDPHAT_FIELD_FAR && s[0] == 0 && s[1] == 0 && s[2] == 0)
+            return fail(SVDPHAT_INVALID_ARG, "zero far-field direction at " + std::to_string(q));
+    }
+    return SVDPHAT_OK;
+}
+
+}  // namespace svdphat
+
+using namespace svdphat;
+
+struct svdphat_plan_s {
+    Plan p;
+    ~svdphat_plan_s() {
+        void* bufs[] = {p.d_W16, p.d_V16, p.d_R16, p.d_rep, p.d_delay, p.d_window, p.d_twN, p.d_P16,
+                        p.d_keys, p.d_Z32, p.d_Zs16, p.d_zflag, p.d_stage, p.d_doa_stage, p.d_score_stage};
+        for (void* b : bufs)
+            if (b) cudaFree(b);
+    }
+};
+
+extern "C" {
+
+const char* svdphat_status_str(svdphat_status s) {
+    switch (s) {
+        case SVDPHAT_OK: return "OK";
+        case SVDPHAT_INVALID_ARG: return "INVALID_ARG";
+        case SVDPHAT_ALLOC: return "ALLOC";
+        case SVDPHAT_CUDA: return "CUDA";
+        case SVDPHAT_NUMERIC: return "NUMERIC";
+        case SVDPHAT_UNSUPPORTED: return "UNSUPPORTED";
+        case SVDPHAT_TOO_LARGE: return "TOO_LARGE";
+    }
+    return "UNKNOWN";
+}
+
+const char* svdphat_last_error(void) { return g_err.c_str(); }
+
+int64_t svdphat_frame_count(int64_t L, int32_t N, int32_t hop) {
+    if (N <= 0 || hop <= 0 || L < N) return 0;
+    return 1 + (L - N) / hop;
+}
+
+void svdphat_plan_destroy(svdphat_plan_t plan) {
+    if (!plan) return;
+    cudaSetDevice(plan->p.device);
+    delete plan;
+}
+
+svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* out) {
+    if (!out) return fail(SVDPHAT_INVALID_ARG, "out is NULL");
+    *out = nullptr;
+    svdphat_status st = validate(d);
+    if (st != SVDPHAT_OK) return st;
+    const auto t0 = std::chrono::steady_clock::now();
+
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(SVDPHAT_UNSUPPORTED, "no CUDA device");
+    if (d->device < 0 || d->device >= ndev) return fail(SVDPHAT_INVALID_ARG, "device ordinal out of range");
+    SVD_CUDA_TRY(cudaSetDevice(d->device));
+    cudaDeviceProp prop;
+    SVD_CUDA_TRY(cudaGetDeviceProperties(&prop, d->device));
+    if (prop.major != 10 || prop.minor != 0)
+        return fail(SVDPHAT_UNSUPPORTED, "libsvdphat is built for sm_100a; device is sm_" +
+                                             std::to_string(prop.major) + std::to_string(prop.minor));
+
+    std::unique_ptr<svdphat_plan_s> h(new svdphat_plan_s());
+    Plan& p = h->p;
+    p.M = d->M;
+    p.N = d->N;
+    p.hop = d->hop;
+    p.Kb = d->N / 2 + 1;
+    p.P = d->M * (d->M - 1) / 2;
+    p.PK = (int64_t)p.P * p.Kb;
+    p.Q = d->Q;
+    p.field = d->field;
+    p.methods = d->methods;
+    p.device = d->device;
+    p.fs = d->fs;
+    p.c = d->c;
+    p.delta = d->delta;
+    p.max_frames = d->max_frames;
+    p.F_pad = std::max<int64_t>(256, (d->max_frames + 255) / 256 * 256);
+    p.L = make_layout(d->M, d->N);
+    p.trace = (double)p.Q * (double)p.P * (double)p.Kb;  // Tr{W W^H}, every |W| = 1 (eq. 4)
+    p.num_sms = prop.multiProcessorCount;
+
+    // ---- TDOAs in samples (float64): eq. 2 (FAR) or eq. 1 (NEAR); arrival delays
+    const int M = p.M, P = p.P, Q = p.Q;
+    const double k = p.fs / p.c;
+    std::vector<double> tau((size_t)Q * P), delay((size_t)Q * M);
+    const double* r = d->mic_xyz;
+    for (int q = 0; q < Q; ++q) {
+        const double* s = d->points_xyz + 3 * (size_t)q;
+        double* dl = &delay[(size_t)q * M];
+        if (p.field == SVDPHAT_FIELD_FAR) {
+            const double nrm = std::sqrt(s[0] * s[0] + s[1] * s[1] + s[2] * s[2]);
+            const double u[3] = {s[0] / nrm, s[1] / nrm, s[2] / nrm};
+            int pp = 0;
+            for (int i = 0; i < M; ++i)
+                for (int j = i + 1; j < M; ++j) {
+                    const double dx = r[3 * j] - r[3 * i], dy = r[3 * j + 1] - r[3 * i + 1],
+                                 dz = r[3 * j + 2] - r[3 * i + 2];
+                    tau[(size_t)q * P + pp++] = k * (dx * u[0] + dy * u[1] + dz * u[2]) + 0.0;  // +0.0: no -0 rows
+                }
+            for (int m = 0; m < M; ++m) dl[m] = -k * (r[3 * m] * u[0] + r[3 * m + 1] * u[1] + r[3 * m + 2] * u[2]);
+        } else {
+            std::vector<double> dist(M);
+            for (int m = 0; m < M; ++m) {
+                const double dx = s[0] - r[3 * m], dy = s[1] - r[3 * m + 1], dz = s[2] - r[3 * m + 2];
+                dist[m] = std::sqrt(dx * dx + dy * dy + dz * dz);
+                dl[m] = k * dist[m];
+            }
+            int pp = 0;
+            for (int i = 0; i < M; ++i)
+                for (int j = i + 1; j < M; ++j) tau[(size_t)q * P + pp++] = k * (dist[i] - dist[j]) + 0.0;
+        }
+        const double mn = *std::min_element(dl, dl + M);
+        for (int m = 0; m < M; ++m) dl[m] -= mn;
+    }
+
+    // ---- steering classes: bitwise-identical tau rows share one W row (R11); rep = lowest index
+    {
+        std::unordered_map<uint64_t, std::vector<int>> buckets;
+        std::vector<int> cls_of(Q, -1);
+        for (int q = 0; q < Q; ++q) {
+            const unsigned char* b = reinterpret_cast<const unsigned char*>(&tau[(size_t)q * P]);
+            uint64_t hsh = 1469598103934665603ull;
+            for (size_t i = 0; i < (size_t)P * 8; ++i) hsh = (hsh ^ b[i]) * 1099511628211ull;
+            auto& v = buckets[hsh];
+            int found = -1;
+            for (int c : v)
+                if (std::memcmp(&tau[(size_t)p.rep_q[c] * P], &tau[(size_t)q * P], (size_t)P * 8) == 0) {
+                    found = c;
+                    break;
+                }
+            if (found < 0) {
+                found = (int)p.rep_q.size();
+                p.rep_q.push_back(q);
+                p.cls_count.push_back(0);
+                v.push_back(found);
+            }
+            p.cls_count[found]++;
+            cls_of[q] = found;
+        }
+    }
+    p.Q_eff = (int)p.rep_q.size();
+    p.Q_pad = (p.Q_eff + 127) / 128 * 128;
+
+    // ---- device tables
+    std::vector<double> tau_cls((size_t)p.Q_eff * P);
+    for (int c = 0; c < p.Q_eff; ++c)
+        std::memcpy(&tau_cls[(size_t)c * P], &tau[(size_t)p.rep_q[c] * P], (size_t)P * 8);
+    double* d_tau = nullptr;
+    SVD_CUDA_TRY(cudaMalloc(&d_tau, tau_cls.size() * 8));
+    std::unique_ptr<double, decltype(&cudaFree)> tau_guard(d_tau, &cudaFree);
+    SVD_CUDA_TRY(cudaMemcpy(d_tau, tau_cls.data(), tau_cls.size() * 8, cudaMemcpyHostToDevice));
+    SVD_CUDA_TRY(cudaMalloc(&p.d_rep, (size_t)p.Q_eff * sizeof(int)));
+    SVD_CUDA_TRY(cudaMemcpy(p.d_rep, p.rep_q.data(), (size_t)p.Q_eff * sizeof(int), cudaMemcpyHostToDevice));
+    {
+        std::vector<float> df(delay.begin(), delay.end());
+        SVD_CUDA_TRY(cudaMalloc(&p.d_delay, df.size() * sizeof(float)));
+        SVD_CUDA_TRY(cudaMemcpy(p.d_delay, df.data(), df.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    {
+        std::vector<float> w(p.N);
+        std::vector<float2> tw(p.N);
+        const double pi = 3.14159265358979323846;
+        for (int n = 0; n < p.N; ++n) {
+            w[n] = (float)std::sin(pi * (n + 0.5) / p.N);  // sine window (reading R1)
+            tw[n] = make_float2((float)std::cos(2 * pi * n / p.N), (float)-std::sin(2 * pi * n / p.N));
+        }
+        SVD_CUDA_TRY(cudaMalloc(&p.d_window, p.N * sizeof(float)));
+        SVD_CUDA_TRY(cudaMemcpy(p.d_window, w.data(), p.N * sizeof(float), cudaMemcpyHostToDevice));
+        SVD_CUDA_TRY(cudaMalloc(&p.d_twN, p.N * sizeof(float2)));
+        SVD_CUDA_TRY(cudaMemcpy(p.d_twN, tw.data(), p.N * sizeof(float2), cudaMemcpyHostToDevice));
+    }
+
+    // ---- operands
+    if (p.methods & SVDPHAT_METHOD_SRP) {
+        st = setup_srp_operand(p, d_tau);
+        if (st != SVDPHAT_OK) return st;
+        if (!encode_2d(&p.tm_W, p.d_W16, p.Q_pad, p.L.K_total, 128))
+            return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(W) failed");
+    }
+    if (p.methods & SVDPHAT_METHOD_SVD) {
+        st = setup_svd_operands(p, d_tau, d->rank_D);
+        if (st != SVDPHAT_OK) return st;
+        if (!encode_2d(&p.tm_V, p.d_V16, 2 * p.Dh, p.L.K_total, 128))
+            return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(V) failed");
+        if (!encode_2d(&p.tm_R, p.d_R16, p.Q_pad, p.K2, 128))
+            return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(R) failed");
+    }
+
+    // ---- workspace for max_frames
+    const int64_t Fp = p.F_pad;
+    const int64_t bytes_P16 = (int64_t)p.L.n_chunks * p.L.Mi * Fp * p.L.unit_bytes;
+    SVD_CUDA_TRY(cudaMalloc(&p.d_P16, bytes_P16));
+    SVD_CUDA_TRY(cudaMemset(p.d_P16, 0, bytes_P16));
+    SVD_CUDA_TRY(cudaMalloc(&p.d_keys, Fp * sizeof(unsigned long long)));
+    p.bytes_ws = bytes_P16 + Fp * 8;
+    if (p.methods & SVDPHAT_METHOD_SVD) {
+        SVD_CUDA_TRY(cudaMalloc(&p.d_Z32, Fp * 2 * p.Dh * sizeof(float)));
+        SVD_CUDA_TRY(cudaMemset(p.d_Z32, 0, Fp * 2 * p.Dh * sizeof(float)));
+        SVD_CUDA_TRY(cudaMalloc(&p.d_Zs16, Fp * p.K2 * 2));
+        SVD_CUDA_TRY(cudaMemset(p.d_Zs16, 0, Fp * p.K2 * 2));
+        SVD_CUDA_TRY(cudaMalloc(&p.d_zflag, Fp * sizeof(int)));
+        SVD_CUDA_TRY(cudaMemset(p.d_zflag, 0, Fp * sizeof(int)));
+        p.bytes_ws += Fp * 2 * p.Dh * 4 + Fp * p.K2 * 2 + Fp * 4;
+        if (!encode_2d(&p.tm_Zs, p.d_Zs16, Fp, p.K2, 256))
+            return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(Zs) failed");
+    }
+    SVD_CUDA_TRY(gemm_set_attributes());
+    SVD_CUDA_TRY(cudaDeviceSynchronize());
+    p.setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    *out = h.release();
+    return SVDPHAT_OK;
+}
+
+svdphat_status svdphat_plan_info(svdphat_plan_t plan, svdphat_plan_info_t* out) {
+    if (!plan || !out) return fail(SVDPHAT_INVALID_ARG, "NULL argument");
+    const Plan& p = plan->p;
+    std::memset(out, 0, sizeof(*out));
+    out->M = p.M;
+    out->P = p.P;
+    out->N = p.N;
+    out->K_bins = p.Kb;
+    out->PK = p.PK;
+    out->Q = p.Q;
+    out->Q_classes = p.Q_eff;
+    out->D = p.D;
+    out->energy_kept = p.energy_kept;
+    out->trace_WWH = p.trace;
+    out->methods = p.methods;
+    out->gemm_k = (int32_t)p.L.K_total;
+    out->max_frames = p.max_frames;
+    out->bytes_W = p.bytes_W;
+    out->bytes_V = p.bytes_V;
+    out->bytes_R = p.bytes_R;
+    out->bytes_workspace = p.bytes_ws;
+    out->setup_seconds = p.setup_seconds;
+    return SVDPHAT_OK;
+}
+
+svdphat_status svdphat_plan_sigma2(svdphat_plan_t plan, double* out, int32_t n) {
+    if (!plan || !out || n < 0) return fail(SVDPHAT_INVALID_ARG, "NULL argument");
+    const Plan& p = plan->p;
+    if (!(p.methods & SVDPHAT_METHOD_SVD)) return fail(SVDPHAT_INVALID_ARG, "SVD was not planned");
+    const int m = std::min<int>(n, (int)p.sigma2.size());
+    std::memcpy(out, p.sigma2.data(), (size_t)m * sizeof(double));
+    return SVDPHAT_OK;
+}
+
+svdphat_status svdphat_localize(svdphat_plan_t plan, int32_t method, const float* d_audio, int64_t n_frames,
+                                int64_t channel_stride, int64_t frame_stride, int32_t* d_doa, float* d_score,
+                                void* stream) {
+    if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
+    Plan& p = plan->p;
+    if (method != SVDPHAT_METHOD_SRP && method != SVDPHAT_METHOD_SVD)
+        return fail(SVDPHAT_INVALID_ARG, "method must be SRP or SVD");
+    if (!(p.methods & method)) return fail(SVDPHAT_INVALID_ARG, "method was not planned");
+    if (n_frames < 0 || n_frames > p.max_frames) return fail(SVDPHAT_INVALID_ARG, "n_frames out of [0, max_frames]");
+    if (n_frames == 0) return SVDPHAT_OK;
+    if (!d_audio || !d_doa || !d_score) return fail(SVDPHAT_INVALID_ARG, "NULL buffer");
+    if (channel_stride < 0 || frame_stride < 0) return fail(SVDPHAT_INVALID_ARG, "negative stride");
+    if (reinterpret_cast<uintptr_t>(d_audio) & 3) return fail(SVDPHAT_INVALID_ARG, "d_audio not 4-byte aligned");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int F = (int)n_frames;
+    SVD_CUDA_TRY(cudaSetDevice(p.device));
+    SVD_CUDA_TRY(launch_stft_phat(p, d_audio, channel_stride, frame_stride, F, s));
+    SVD_CUDA_TRY(cudaMemsetAsync(p.d_keys, 0, (size_t)F * 8, s));
+    if (method == SVDPHAT_METHOD_SRP) {
+        SVD_CUDA_TRY(launch_gemm(p, 0, F, s));
+    } else {
+        SVD_CUDA_TRY(launch_gemm(p, 1, F, s));
+        SVD_CUDA_TRY(launch_zsplit(p, F, s));
+        SVD_CUDA_TRY(launch_gemm(p, 2, F, s));
+    }
+    SVD_CUDA_TRY(launch_finalize(p, method, F, d_doa, d_score, s));
+    p.last_frames = F;
+    p.last_method = method;
+    return SVDPHAT_OK;
+}
+
+svdphat_status svdphat_localize_host(svdphat_plan_t plan, int32_t method, const float* h_audio, int64_t audio_elems,
+                                     int64_t n_frames, int64_t channel_stride, int64_t frame_stride, int32_t* h_doa,
+                                     float* h_score, void* stream) {
+    if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
+    Plan& p = plan->p;
+    if (n_frames < 0 || n_frames > p.max_frames) return fail(SVDPHAT_INVALID_ARG, "n_frames out of [0, max_frames]");
+    if (n_frames == 0) return SVDPHAT_OK;
+    if (!h_audio || !h_doa || !h_score || audio_elems <= 0) return fail(SVDPHAT_INVALID_ARG, "NULL/empty buffer");
+    const int64_t need = (int64_t)(p.M - 1) * channel_stride + (n_frames - 1) * frame_stride + p.N;
+    if (need > audio_elems) return fail(SVDPHAT_INVALID_ARG, "audio buffer smaller than the addressed frames");
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    SVD_CUDA_TRY(cudaSetDevice(p.device));
+    if (audio_elems > p.stage_elems) {
+        if (p.d_stage) cudaFree(p.d_stage);
+        p.d_stage = nullptr;
+        p.stage_elems = 0;
+        if (cudaMalloc(&p.d_stage, audio_elems * sizeof(float)) != cudaSuccess)
+            return fail(SVDPHAT_ALLOC, "staging buffer allocation failed");
+        p.stage_elems = audio_elems;
+    }
+    if (!p.d_doa_stage) {
+        if (cudaMalloc(&p.d_doa_stage, p.F_pad * sizeof(int32_t)) != cudaSuccess ||
+            cudaMalloc(&p.d_score_stage, p.F_pad * sizeof(float)) != cudaSuccess)
+            return fail(SVDPHAT_ALLOC, "result staging allocation failed");
+    }
+    SVD_CUDA_TRY(cudaMemcpyAsync(p.d_stage, h_audio, audio_elems * sizeof(float), cudaMemcpyHostToDevice, s));
+    svdphat_status st = svdphat_localize(plan, method, p.d_stage, n_frames, channel_stride, frame_stride,
+                                         p.d_doa_stage, p.d_score_stage, stream);
+    if (st != SVDPHAT_OK) return st;
+    SVD_CUDA_TRY(cudaMemcpyAsync(h_doa, p.d_doa_stage, n_frames * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SVD_CUDA_TRY(cudaMemcpyAsync(h_score, p.d_score_stage, n_frames * sizeof(float), cudaMemcpyDeviceToHost, s));
+    SVD_CUDA_TRY(cudaStreamSynchronize(s));
+    return SVDPHAT_OK;
+}
+
+svdphat_status svdphat_debug_dump(svdphat_plan_t plan, int32_t what, int64_t n_frames, void* host_out, int64_t bytes) {
+    if (!plan || !host_out) return fail(SVDPHAT_INVALID_ARG, "NULL argument");
+    Plan& p = plan->p;
+    SVD_CUDA_TRY(cudaSetDevice(p.device));
+    SVD_CUDA_TRY(cudaDeviceSynchronize());
+    if (n_frames < 0 || n_frames > p.last_frames) return fail(SVDPHAT_INVALID_ARG, "n_frames > frames of last call");
+    const int F = (int)n_frames;
+    if (what == SVDPHAT_DUMP_CLASS_REP) {
+        if (bytes < (int64_t)p.Q_eff * 4) return fail(SVDPHAT_INVALID_ARG, "buffer too small");
+        std::memcpy(host_out, p.rep_q.data(), (size_t)p.Q_eff * 4);
+        return SVDPHAT_OK;
+    }
+    if (what == SVDPHAT_DUMP_KEYS) {
+        if (bytes < (int64_t)F * 8) return fail(SVDPHAT_INVALID_ARG, "buffer too small");
+        SVD_CUDA_TRY(cudaMemcpy(host_out, p.d_keys, (size_t)F * 8, cudaMemcpyDeviceToHost));
+        return SVDPHAT_OK;
+    }
+    if (what == SVDPHAT_DUMP_Z) {
+        if (!p.d_Z32) return fail(SVDPHAT_INVALID_ARG, "SVD not planned");
+        if (bytes < (int64_t)F * 2 * p.D * 4) return fail(SVDPHAT_INVALID_ARG, "buffer too small");
+        std::vector<float> z((size_t)F * 2 * p.Dh);
+        SVD_CUDA_TRY(cudaMemcpy(z.data(), p.d_Z32, z.size() * 4, cudaMemcpyDeviceToHost));
+        float* o = static_cast<float*>(host_out);
+        for (int f = 0; f < F; ++f)
+            for (int d = 0; d < p.D; ++d) {
+                o[((size_t)f * 2 * p.D) + d] = z[(size_t)f * 2 * p.Dh + d];
+                o[((size_t)f * 2 * p.D) + p.D + d] = z[(size_t)f * 2 * p.Dh + p.Dh + d];
+            }
+        return SVDPHAT_OK;
+    }
+    if (what == SVDPHAT_DUMP_PHASORS) {
+        if (bytes < (int64_t)F * p.M * p.Kb * 2 * 4) return fail(SVDPHAT_INVALID_ARG, "buffer too small");
+        const int64_t nb = (int64_t)p.L.n_chunks * p.L.Mi * p.F_pad * p.L.unit_bytes;
+        std::vector<__half> h((size_t)nb / 2);
+        SVD_CUDA_TRY(cudaMemcpy(h.data(), p.d_P16, nb, cudaMemcpyDeviceToHost));
+        float* o = static_cast<float*>(host_out);
+        const int bpc = p.L.bpc;
+        for (int f = 0; f < F; ++f)
+            for (int m = 0; m < p.M; ++m)
+                for (int kb = 0; kb < p.Kb; ++kb) {
+                    const int c = kb / bpc, s = kb % bpc;
+                    const size_t rec = (((size_t)c * p.L.Mi + m) * p.F_pad + f) * (size_t)(bpc * 2);
+                    o[(((size_t)f * p.M + m) * p.Kb + kb) * 2 + 0] = __half2float(h[rec + s]);
+                    o[(((size_t)f * p.M + m) * p.Kb + kb) * 2 + 1] = __half2float(h[rec + bpc + s]);
+                }
+        return SVDPHAT_OK;
+    }
+    return fail(SVDPHAT_INVALID_ARG, "unknown dump id");
+}
+
+}  // extern "C"

@@ -1,0 +1,390 @@
+// gemm_tc.cu — the projection GEMMs of SRP-PHAT and SVD-PHAT on the 5th-generation tensor cores (tcgen05).
+//
+//   mode 0 (SRP, eq. 9):   Y[q,f] = Re{W_q . X_f} = sum_kappa W16[q,kappa] * x16[f,kappa]
+//                                        + fused argmax over q (eq. 6), lowest index on ties.
+//   mode 1 (SVD, eq. 12):  [Z_r; Z_i][d,f] = sum_kappa V16[d,kappa] * x16[f,kappa]   -> Z32
+//   mode 2 (SVD, eqs. 14-15): s[q,f] = Re{Dhat_q . Zhat_f} over split-FP16 operands
+//                                        + fused argmax over q.
+//
+// A operand (M side, 128 rows per tile) = W16 / V16 / R16 streamed by TMA (SWIZZLE_128B, K-major).
+// B operand (N side, 256 frames per tile) = in modes 0/1 the PHAT cross-spectrum X (eqs. 3, 7) built in shared
+// memory by 8 producer warps from the per-channel unit phasors (it never exists in HBM); in mode 2 Zhat via TMA.
+// Accumulators: FP32 in TMEM, two 256-column buffers so the epilogue of tile t overlaps the MMAs of tile t+1.
+// Warp roles: 0 TMA, 1 MMA issuer (one thread), 2..5 epilogue (TMEM lane groups 2,3,0,1), 6..13 producer.
+#include <cuda_fp16.h>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace svdphat {
+
+constexpr int BM = 128;                    // tile rows (A)
+constexpr int BN = 256;                    // tile frames (B)
+constexpr int BK = 64;                     // fp16 per slab row = 128 B = one swizzle atom row
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;       // 16 KB
+constexpr int B_BYTES = BN * BK * 2;       // 32 KB
+constexpr int NUM_PRODUCER_WARPS = 8;
+constexpr int SMEM_BYTES = 1024 + STAGES * (A_BYTES + B_BYTES) + 256;
+
+struct GemmParams {
+    const uint8_t* P16;                    // phasors (modes 0/1)
+    int F;                                 // valid frames
+    int F_pad;
+    int n_chunks;
+    int n_slabs;                           // K / 64
+    int m_tiles, n_tiles;
+    int rows_valid;                        // rows of A that are real (mask for the argmax / store)
+    unsigned long long* keys;              // argmax keys [F]
+    float* Z;                              // mode 1 output [F_pad][ldz]
+    int ldz;
+};
+
+// ---------------------------------------------------------------- compile-time pair enumeration over Mi mics
+template <int Mi>
+struct PairTab {
+    int i[Mi * (Mi - 1) / 2 + 1];
+    int j[Mi * (Mi - 1) / 2 + 1];
+    constexpr PairTab() : i(), j() {
+        int p = 0;
+        for (int a = 0; a < Mi; ++a)
+            for (int b = a + 1; b < Mi; ++b) {
+                i[p] = a;
+                j[p] = b;
+                ++p;
+            }
+    }
+};
+
+__device__ __forceinline__ uint32_t h2mul(uint32_t a, uint32_t b) {
+    __half2 r = __hmul2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b));
+    return *reinterpret_cast<uint32_t*>(&r);
+}
+__device__ __forceinline__ uint32_t h2fma(uint32_t a, uint32_t b, uint32_t c) {
+    __half2 r = __hfma2(*reinterpret_cast<__half2*>(&a), *reinterpret_cast<__half2*>(&b),
+                        *reinterpret_cast<__half2*>(&c));
+    return *reinterpret_cast<uint32_t*>(&r);
+}
+
+// u64 max-reduce of 32 columns across the 32 lanes of a warp; afterwards lane l holds column l's maximum.
+__device__ __forceinline__ unsigned long long transpose_max32(unsigned long long (&k)[32], int lane) {
+#pragma unroll
+    for (int h = 16; h >= 1; h >>= 1) {
+        const bool upper = (lane & h) != 0;
+#pragma unroll
+        for (int c = 0; c < h; ++c) {
+            unsigned long long send = upper ? k[c] : k[c + h];
+            unsigned long long mine = upper ? k[c + h] : k[c];
+            unsigned long long recv = __shfl_xor_sync(0xffffffffu, send, h);
+            k[c] = mine > recv ? mine : recv;
+        }
+    }
+    return k[0];
+}
+
+template <int Mi, int BPC, int MODE>
+__global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
+    gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+    constexpr bool kProducer = (MODE != 2);
+    constexpr int kPairs = Mi * (Mi - 1) / 2;
+    constexpr int kUnitsRaw = (BPC == 4) ? kPairs : (kPairs + 1) / 2;
+    constexpr int kU = (kUnitsRaw + 7) / 8 * 8;        // units per chunk
+    constexpr uint32_t kIdesc = umma_idesc_f16(BM, BN);
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES * A_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES * B_BYTES);
+    uint64_t* empty = full + STAGES;
+    uint64_t* tfull = empty + STAGES;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int n_tiles_total = p.m_tiles * p.n_tiles;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], kProducer ? 1 + NUM_PRODUCER_WARPS : 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 4);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) {
+        tmem_alloc<512>(tmem_slot);
+    }
+    if (warp == 1 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        if (!kProducer) tma_prefetch_desc(&tmB);
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        // ============================================================ TMA producer (A, and B in mode 2)
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint32_t bytes = kProducer ? A_BYTES : (A_BYTES + B_BYTES);
+            for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+                const int m = t / p.n_tiles, n = t % p.n_tiles;
+                for (int ks = 0; ks < p.n_slabs; ++ks) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], bytes);
+                    tma_load_2d(sA + stage * A_BYTES, &tmA, ks * BK, m * BM, &full[stage]);
+                    if (!kProducer) tma_load_2d(sB + stage * B_BYTES, &tmB, ks * BK, n * BN, &full[stage]);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ============================================================ MMA issuer
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+            mbar_wait(&tempty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + acc * BN;
+            for (int ks = 0; ks < p.n_slabs; ++ks) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
+                    const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+#pragma unroll
+                    for (int kk = 0; kk < BK / 16; ++kk) {
+                        umma_f16(d_tmem, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), kIdesc,
+                                 (ks | kk) != 0);
+                    }
+                    umma_commit(&empty[stage]);
+                }
+                __syncwarp();
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            if (lane == 0) umma_commit(&tfull[acc]);
+            __syncwarp();
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    } else if (warp < 6) {
+        // ============================================================ epilogue: TMEM -> registers -> argmax / Z
+        const int g = warp & 3;                                    // TMEM lane group this warp may access
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+            const int m = t / p.n_tiles, n = t % p.n_tiles;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int row = m * BM + g * 32 + lane;
+            const bool row_ok = row < p.rows_valid;
+#pragma unroll 1
+            for (int j0 = 0; j0 < BN; j0 += 32) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + acc * BN + j0, r);
+                tmem_ld_wait();
+                const int f0 = n * BN + j0;
+                if (MODE == 1) {
+                    if (row_ok) {
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) {
+                            if (f0 + jj < p.F) p.Z[(int64_t)(f0 + jj) * p.ldz + row] = __uint_as_float(r[jj]);
+                        }
+                    }
+                } else {
+                    unsigned long long k[32];
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj) {
+                        const float v = __uint_as_float(r[jj]);
+                        k[jj] = (row_ok && v == v) ? make_key(v, (uint32_t)row) : 0ull;
+                    }
+                    const unsigned long long best = transpose_max32(k, lane);
+                    if (f0 + lane < p.F && best != 0ull) atomicMax(&p.keys[f0 + lane], best);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    } else if (kProducer) {
+        // ============================================================ B producer: X (eqs. 3, 7) from phasors
+        constexpr PairTab<Mi> PT{};
+        const int tp = (warp - 6) * 32 + lane;                    // frame row of the B tile: 0..255
+        const uint32_t row_off = (uint32_t)((tp >> 3) * 1024 + (tp & 7) * 128);
+        const uint32_t xr = (uint32_t)(tp & 7);
+        int stage = 0;
+        uint32_t phase = 0;
+        constexpr int kUB = BPC * 4;                               // bytes per phasor record: bpc*2 halves
+        for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
+            const int n = t % p.n_tiles;
+            const int f = n * BN + tp;
+            const bool valid = f < p.F;
+#pragma unroll 1
+            for (int c = 0; c < p.n_chunks; ++c) {
+                // e[m][w]: BPC=4 -> {Re k0k1, Re k2k3, Im k0k1, Im k2k3}; BPC=2 -> {Re k0k1, Im k0k1}
+                uint32_t e[Mi][BPC];
+                const uint8_t* src = p.P16 + ((int64_t)c * Mi * p.F_pad + f) * kUB;
+#pragma unroll
+                for (int m = 0; m < Mi; ++m) {
+                    if (BPC == 4) {
+                        uint4 v = valid ? __ldg(reinterpret_cast<const uint4*>(src + (int64_t)m * p.F_pad * kUB))
+                                        : make_uint4(0, 0, 0, 0);
+                        e[m][0] = v.x;
+                        e[m][1] = v.y;
+                        e[m][2 % BPC] = v.z;
+                        e[m][3 % BPC] = v.w;
+                    } else {
+                        uint2 v = valid ? __ldg(reinterpret_cast<const uint2*>(src + (int64_t)m * p.F_pad * kUB))
+                                        : make_uint2(0, 0);
+                        e[m][0] = v.x;
+                        e[m][1] = v.y;
+                    }
+                }
+                uint32_t outw[4];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    if ((u & 7) == 0) mbar_wait(&empty[stage], phase ^ 1);
+                    if (BPC == 4) {
+                        if (u < kPairs) {
+                            const int a = PT.i[u], b = PT.j[u];
+                            // x = e_a conj(e_b): Re = ra rb + ia ib, Im = ia rb - ra ib   (eq. 3)
+                            const uint32_t nra01 = e[a][0] ^ 0x80008000u, nra23 = e[a][1 % BPC] ^ 0x80008000u;
+                            outw[0] = h2fma(e[a][0], e[b][0], h2mul(e[a][2 % BPC], e[b][2 % BPC]));
+                            outw[1] = h2fma(e[a][1 % BPC], e[b][1 % BPC], h2mul(e[a][3 % BPC], e[b][3 % BPC]));
+                            outw[2] = h2fma(e[a][2 % BPC], e[b][0], h2mul(nra01, e[b][2 % BPC]));
+                            outw[3] = h2fma(e[a][3 % BPC], e[b][1 % BPC], h2mul(nra23, e[b][3 % BPC]));
+                        } else {
+                            outw[0] = outw[1] = outw[2] = outw[3] = 0u;
+                        }
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int pp = 2 * u + h;
+                            if (pp < kPairs) {
+                                const int a = PT.i[pp], b = PT.j[pp];
+                                const uint32_t nra = e[a][0] ^ 0x80008000u;
+                                outw[2 * h + 0] = h2fma(e[a][0], e[b][0], h2mul(e[a][1], e[b][1]));
+                                outw[2 * h + 1] = h2fma(e[a][1], e[b][0], h2mul(nra, e[b][1]));
+                            } else {
+                                outw[2 * h + 0] = outw[2 * h + 1] = 0u;
+                            }
+                        }
+                    }
+                    const uint32_t dst = smem_u32(sB + stage * B_BYTES) + row_off + ((((uint32_t)u & 7u) ^ xr) << 4);
+                    st_shared_v4(dst, outw[0], outw[1], outw[2], outw[3]);
+                    if ((u & 7) == 7) {
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&full[stage]);
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc<512>(tmem_base);
+    }
+}
+
+// ---------------------------------------------------------------- host side
+template <int Mi, int BPC, int MODE>
+static cudaError_t set_attr_one() {
+    return cudaFuncSetAttribute(gemm_kernel<Mi, BPC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                SMEM_BYTES);
+}
+
+cudaError_t gemm_set_attributes() {
+    cudaError_t e = cudaSuccess;
+#define SVD_ATTR(MI, B)                                        \
+    if ((e = set_attr_one<MI, B, 0>()) != cudaSuccess) return e; \
+    if ((e = set_attr_one<MI, B, 1>()) != cudaSuccess) return e;
+    SVD_ATTR(4, 4)
+    SVD_ATTR(8, 4)
+    SVD_ATTR(16, 4)
+    SVD_ATTR(32, 2)
+#undef SVD_ATTR
+    return set_attr_one<4, 4, 2>();
+}
+
+template <int Mi, int BPC, int MODE>
+static cudaError_t launch_one(const CUtensorMap& A, const CUtensorMap& B, const GemmParams& gp, int grid,
+                              cudaStream_t s) {
+    gemm_kernel<Mi, BPC, MODE><<<grid, 32 * (6 + NUM_PRODUCER_WARPS), SMEM_BYTES, s>>>(A, B, gp);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
+    GemmParams gp{};
+    gp.P16 = p.d_P16;
+    gp.F = F;
+    gp.F_pad = (int)p.F_pad;
+    gp.n_chunks = p.L.n_chunks;
+    gp.n_tiles = (F + BN - 1) / BN;
+    gp.keys = p.d_keys;
+    gp.Z = p.d_Z32;
+    gp.ldz = 2 * p.Dh;
+    const CUtensorMap* A = nullptr;
+    const CUtensorMap* B = &p.tm_W;  // unused placeholder for producer modes
+    if (mode == 0) {
+        A = &p.tm_W;
+        gp.n_slabs = (int)(p.L.K_total / BK);
+        gp.m_tiles = p.Q_pad / BM;
+        gp.rows_valid = p.Q_eff;
+    } else if (mode == 1) {
+        A = &p.tm_V;
+        gp.n_slabs = (int)(p.L.K_total / BK);
+        gp.m_tiles = (2 * p.Dh) / BM;
+        gp.rows_valid = 2 * p.Dh;
+    } else {
+        A = &p.tm_R;
+        B = &p.tm_Zs;
+        gp.n_slabs = p.K2 / BK;
+        gp.m_tiles = p.Q_pad / BM;
+        gp.rows_valid = p.Q_eff;
+    }
+    const int tiles = gp.m_tiles * gp.n_tiles;
+    const int grid = tiles < p.num_sms ? tiles : p.num_sms;
+    if (tiles == 0) return cudaSuccess;
+    if (mode == 2) return launch_one<4, 4, 2>(*A, *B, gp, grid, s);
+#define SVD_DISPATCH(MI, BP)                                                                      \
+    if (p.L.Mi == MI) {                                                                          \
+        return mode == 0 ? launch_one<MI, BP, 0>(*A, *B, gp, grid, s) : launch_one<MI, BP, 1>(*A, *B, gp, grid, s); \
+    }
+    SVD_DISPATCH(4, 4)
+    SVD_DISPATCH(8, 4)
+    SVD_DISPATCH(16, 4)
+    SVD_DISPATCH(32, 2)
+#undef SVD_DISPATCH
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace svdphat

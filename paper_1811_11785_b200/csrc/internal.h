@@ -1,0 +1,104 @@
+// internal.h — plan structure and kernel launchers of libsvdphat (not part of the public ABI).
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/svdphat.h"
+
+namespace svdphat {
+
+// ---------------------------------------------------------------- device data layout
+// The GEMM contraction index kappa runs over (chunk c, unit u, slot s):  kappa = ((c*U + u)*8 + s).
+//   bpc = 4 (M' <= 16): unit = one pair p = u; slots 0..3 = Re of bins 4c..4c+3, 4..7 = Im of the same bins.
+//   bpc = 2 (M' = 32) : unit = pairs 2u, 2u+1; slots {0,1} Re p=2u bins 2c,2c+1; {2,3} Im p=2u; {4,5} Re p=2u+1;
+//                       {6,7} Im p=2u+1.
+// Pairs are enumerated lexicographically over M' >= M "instantiated" mics; pairs touching a mic >= M, bins
+// >= N/2+1 and units >= pairs are zero.  Phasors live in P16[c][m][F_pad][bpc*2 halves] (Re bins | Im bins).
+struct Layout {
+    int M = 0, Mi = 0;        // real mics, instantiated mics (kernel template)
+    int P = 0, Pi = 0;        // real pairs, instantiated pairs
+    int N = 0, Kb = 0;        // frame size, bins N/2+1
+    int bpc = 4;              // bins per chunk
+    int n_chunks = 0;         // ceil(Kb / bpc)
+    int U = 0;                // units per chunk (multiple of 8)
+    int64_t K_total = 0;      // n_chunks * U * 8  (multiple of 64)
+    int unit_bytes = 16;      // bytes of one phasor record (bpc*2 halves)
+};
+
+struct Plan {
+    // description
+    int M = 0, P = 0, N = 0, hop = 0, Kb = 0, field = 0, Q = 0, methods = 0, device = 0;
+    int64_t PK = 0, max_frames = 0, F_pad = 0;
+    double fs = 0, c = 0, delta = 0;
+    Layout L;
+    // steering classes (bitwise-identical tau rows; R11)
+    int Q_eff = 0, Q_pad = 0;
+    std::vector<int> rep_q;       // [Q_eff] lowest point index of each class
+    std::vector<int> cls_count;   // [Q_eff]
+    // SVD
+    int D = 0, Dh = 0, K2 = 0;    // rank, rank padded to 64, search contraction length 3*2*Dh
+    double energy_kept = 0, trace = 0;
+    std::vector<double> sigma2;   // descending
+    double setup_seconds = 0;
+    // device operands (owned)
+    __half* d_W16 = nullptr;      // [Q_pad][K_total]
+    __half* d_V16 = nullptr;      // [2*Dh][K_total]
+    __half* d_R16 = nullptr;      // [Q_pad][K2]
+    int* d_rep = nullptr;         // [Q_eff]
+    float* d_delay = nullptr;     // [Q][M]  relative arrival delays (samples)
+    float* d_window = nullptr;    // [N]
+    float2* d_twN = nullptr;      // [N]     e^{-j 2 pi k / N}
+    // workspace
+    uint8_t* d_P16 = nullptr;     // phasors
+    unsigned long long* d_keys = nullptr;  // [F_pad]
+    float* d_Z32 = nullptr;       // [F_pad][2*Dh]
+    __half* d_Zs16 = nullptr;     // [F_pad][K2]
+    int* d_zflag = nullptr;       // [F_pad]
+    int64_t bytes_W = 0, bytes_V = 0, bytes_R = 0, bytes_ws = 0;
+    // TMA descriptors
+    alignas(64) CUtensorMap tm_W;
+    alignas(64) CUtensorMap tm_V;
+    alignas(64) CUtensorMap tm_R;
+    alignas(64) CUtensorMap tm_Zs;
+    int num_sms = 148;
+    // host-buffer path
+    float* d_stage = nullptr;
+    int64_t stage_elems = 0;
+    int32_t* d_doa_stage = nullptr;
+    float* d_score_stage = nullptr;
+    int64_t last_frames = 0;
+    int last_method = 0;
+};
+
+// ---------------------------------------------------------------- error plumbing
+void set_error(const std::string& msg);
+#define SVD_CUDA_TRY(expr)                                                                                    \
+    do {                                                                                                      \
+        cudaError_t _e = (expr);                                                                              \
+        if (_e != cudaSuccess) {                                                                              \
+            ::svdphat::set_error(std::string(#expr) + ": " + cudaGetErrorString(_e) + " @" __FILE__ ":" +     \
+                                 std::to_string(__LINE__));                                                   \
+            return SVDPHAT_CUDA;                                                                              \
+        }                                                                                                     \
+    } while (0)
+
+// ---------------------------------------------------------------- launchers (return cudaError_t)
+cudaError_t launch_stft_phat(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F,
+                             cudaStream_t s);
+// mode: 0 = SRP argmax (A = W16, B = producer), 1 = SVD GEMM1 store Z (A = V16, B = producer),
+//       2 = SVD search argmax (A = R16, B = Zs16 via TMA)
+cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s);
+cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s);
+cudaError_t launch_finalize(const Plan& p, int method, int F, int32_t* doa, float* score, cudaStream_t s);
+cudaError_t gemm_set_attributes();
+
+// setup (float64, device)
+svdphat_status setup_srp_operand(Plan& p, const double* d_tau_cls);
+svdphat_status setup_svd_operands(Plan& p, const double* d_tau_cls, int rank_D);
+
+}  // namespace svdphat

@@ -1,0 +1,331 @@
+// setup.cu — Alg. 1 offline in float64, run once per plan on the device.
+//
+//  * W16 : W_{q,i,j}[k] = exp(+j 2 pi k tau_{q,i,j} / N) (eq. 4) packed real-split FP16 as
+//          [Re W | -Im W] in the GEMM contraction order (internal.h), one row per steering class.
+//  * SVD : sigma^2 and U from the Hermitian Gram G = W W^H (same singular values / left vectors as eq. 10),
+//          with G built in closed form: G_ab = sum_p sum_{k<Kb} e^{j 2 pi k (tau_ap - tau_bp)/N}
+//          = sum_p e^{j pi (Kb-1) x} sin(pi Kb x) / sin(pi x),  x = (tau_ap - tau_bp)/N  (geometric series).
+//          Twin classes (bitwise-identical rows, R11) enter with multiplicity n_c:  G' = N^1/2 G_r N^1/2
+//          has the spectrum of the full W W^H.  Rank D by eq. 11 with Tr{W W^H} = Q P Kb exactly.
+//          V_D = W^H U_D S_D^{-1} (eq. 10) formed column-chunk-wise with cuBLAS ZGEMM on generated W chunks.
+//          Dictionary rows D_q = (U S)_q (eq. 13) normalised -> split FP16 [hi | lo | hi].
+#include <cublas_v2.h>
+#include <cuda_fp16.h>
+#include <cusolverDn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+
+namespace svdphat {
+
+// kappa index of (instantiated pair pi, bin k, imaginary?) in the GEMM contraction order
+__host__ __device__ __forceinline__ int64_t kappa_of(int pi, int k, int im, int bpc, int U) {
+    const int c = k / bpc, s = k % bpc;
+    if (bpc == 4) return ((int64_t)c * U + pi) * 8 + (im ? 4 : 0) + s;
+    return ((int64_t)c * U + (pi >> 1)) * 8 + (pi & 1) * 4 + (im ? 2 : 0) + s;
+}
+
+// instantiated pair index of real pair (i, j) in the lexicographic enumeration over Mi mics
+__host__ __device__ __forceinline__ int pair_index(int i, int j, int Mi) {
+    return i * (2 * Mi - i - 1) / 2 + (j - i - 1);
+}
+
+// one thread per (class row, real pair): all bins of that pair
+__global__ void pack_w16_kernel(const double* __restrict__ tau, int Q_eff, int P, int M, int Mi, int N, int Kb,
+                                int bpc, int U, int64_t K_total, __half* __restrict__ W16) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= (int64_t)Q_eff * P) return;
+    const int row = (int)(tid / P), p = (int)(tid % P);
+    // real pair p -> (i, j) over M mics
+    int i = 0, rem = p;
+    while (rem >= M - 1 - i) {
+        rem -= M - 1 - i;
+        ++i;
+    }
+    const int j = i + 1 + rem;
+    const int pi = pair_index(i, j, Mi);
+    const double t = tau[(int64_t)row * P + p];
+    __half* dst = W16 + (int64_t)row * K_total;
+    for (int k = 0; k < Kb; ++k) {
+        double s, c;
+        sincospi(2.0 * (double)k * t / (double)N, &s, &c);  // e^{j 2 pi k tau / N}
+        dst[kappa_of(pi, k, 0, bpc, U)] = __double2half(c);
+        dst[kappa_of(pi, k, 1, bpc, U)] = __double2half(-s);
+    }
+}
+
+// lower triangle (column-major) of G' = diag(sqrt n) G_r diag(sqrt n), G_r[a][b] = sum_p Dirichlet(tau_a - tau_b)
+__global__ void gram_kernel(const double* __restrict__ tau, const int* __restrict__ cnt, int n, int P, int N, int Kb,
+                            cuDoubleComplex* __restrict__ G) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = blockIdx.y;
+    if (a >= n || a < b) return;
+    double re = 0.0, im = 0.0;
+    const double* ta = tau + (int64_t)a * P;
+    const double* tb = tau + (int64_t)b * P;
+    for (int p = 0; p < P; ++p) {
+        const double x = (ta[p] - tb[p]) / (double)N;
+        if (x == 0.0) {
+            re += (double)Kb;
+        } else {
+            const double amp = sinpi((double)Kb * x) / sinpi(x);
+            double s, c;
+            sincospi((double)(Kb - 1) * x, &s, &c);
+            re += amp * c;
+            im += amp * s;
+        }
+    }
+    const double w = sqrt((double)cnt[a] * (double)cnt[b]);
+    G[(int64_t)b * n + a] = make_cuDoubleComplex(w * re, w * im);
+}
+
+// Bmat[a][d] (column-major n x D) = sqrt(n_a) U'[a][jd] / sqrt(lambda_d), jd = n-1-d (eigenvalues ascending)
+__global__ void bmat_kernel(const cuDoubleComplex* __restrict__ Uv, const double* __restrict__ lam,
+                            const int* __restrict__ cnt, int n, int D, cuDoubleComplex* __restrict__ B) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    const int d = blockIdx.y;
+    if (a >= n) return;
+    const int jd = n - 1 - d;
+    const double s = sqrt((double)cnt[a] / lam[jd]);
+    const cuDoubleComplex u = Uv[(int64_t)jd * n + a];
+    B[(int64_t)d * n + a] = make_cuDoubleComplex(s * u.x, s * u.y);
+}
+
+// W chunk, column-major n x C: columns c0..c0+C-1 of eq. 8 (pair-major, bins inner), rows = classes
+__global__ void wchunk_kernel(const double* __restrict__ tau, int n, int P, int N, int Kb, int64_t c0, int C,
+                              cuDoubleComplex* __restrict__ Wc) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    const int cc = blockIdx.y;
+    if (a >= n) return;
+    const int64_t col = c0 + cc;
+    const int p = (int)(col / Kb), k = (int)(col % Kb);
+    double s, c;
+    sincospi(2.0 * (double)k * tau[(int64_t)a * P + p] / (double)N, &s, &c);
+    Wc[(int64_t)cc * n + a] = make_cuDoubleComplex(c, s);
+}
+
+// V chunk (column-major C x D) -> V16 rows: d -> [V_r | V_i] (Z_r), Dh + d -> [-V_i | V_r] (Z_i), scaled by sqrt(PK)
+__global__ void pack_v16_kernel(const cuDoubleComplex* __restrict__ Vc, int C, int D, int Dh, int64_t c0, int M,
+                                int Mi, int Kb, int bpc, int U, int64_t K_total, double scale,
+                                __half* __restrict__ V16) {
+    const int cc = blockIdx.x * blockDim.x + threadIdx.x;
+    const int d = blockIdx.y;
+    if (cc >= C) return;
+    const int64_t col = c0 + cc;
+    const int p = (int)(col / Kb), k = (int)(col % Kb);
+    int i = 0, rem = p;
+    while (rem >= M - 1 - i) {
+        rem -= M - 1 - i;
+        ++i;
+    }
+    const int j = i + 1 + rem;
+    const int pi = pair_index(i, j, Mi);
+    const cuDoubleComplex v = Vc[(int64_t)d * C + cc];
+    const int64_t kr = kappa_of(pi, k, 0, bpc, U), ki = kappa_of(pi, k, 1, bpc, U);
+    __half* zr = V16 + (int64_t)d * K_total;
+    __half* zi = V16 + (int64_t)(Dh + d) * K_total;
+    zr[kr] = __double2half(scale * v.x);
+    zr[ki] = __double2half(scale * v.y);
+    zi[kr] = __double2half(-scale * v.y);
+    zi[ki] = __double2half(scale * v.x);
+}
+
+// R16 row a: Rhat_a = normalise(U'[a][jd] sqrt(lambda_d)) -> [hi(Re) hi(-Im) | lo(Re) lo(-Im) | hi(Re) hi(-Im)]
+__global__ void pack_r16_kernel(const cuDoubleComplex* __restrict__ Uv, const double* __restrict__ lam, int n, int D,
+                                int Dh, int K2, __half* __restrict__ R16) {
+    const int a = blockIdx.x;
+    __shared__ double red[32];
+    double ss = 0.0;
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+        const int jd = n - 1 - d;
+        const cuDoubleComplex u = Uv[(int64_t)jd * n + a];
+        ss += (u.x * u.x + u.y * u.y) * lam[jd];
+    }
+    for (int o = 16; o >= 1; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+        for (int o = 16; o >= 1; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+        if (threadIdx.x == 0) red[0] = v;
+    }
+    __syncthreads();
+    const double inv = 1.0 / sqrt(red[0]);
+    __half* row = R16 + (int64_t)a * K2;
+    const int W2 = 2 * Dh;
+    for (int d = threadIdx.x; d < D; d += blockDim.x) {
+        const int jd = n - 1 - d;
+        const cuDoubleComplex u = Uv[(int64_t)jd * n + a];
+        const double sl = sqrt(lam[jd]) * inv;
+        const float vr = (float)(u.x * sl), vi = (float)(-u.y * sl);  // [Re R | -Im R]
+        const __half hr = __float2half_rn(vr), hi = __float2half_rn(vi);
+        const __half lr = __float2half_rn(vr - __half2float(hr)), li = __float2half_rn(vi - __half2float(hi));
+        row[d] = hr;
+        row[Dh + d] = hi;
+        row[W2 + d] = lr;
+        row[W2 + Dh + d] = li;
+        row[2 * W2 + d] = hr;
+        row[2 * W2 + Dh + d] = hi;
+    }
+}
+
+static inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
+
+svdphat_status setup_srp_operand(Plan& p, const double* d_tau_cls) {
+    p.bytes_W = (int64_t)p.Q_pad * p.L.K_total * 2;
+    SVD_CUDA_TRY(cudaMalloc(&p.d_W16, p.bytes_W));
+    SVD_CUDA_TRY(cudaMemset(p.d_W16, 0, p.bytes_W));
+    const int64_t n = (int64_t)p.Q_eff * p.P;
+    pack_w16_kernel<<<cdiv(n, 256), 256>>>(d_tau_cls, p.Q_eff, p.P, p.M, p.L.Mi, p.N, p.Kb, p.L.bpc, p.L.U,
+                                           p.L.K_total, p.d_W16);
+    SVD_CUDA_TRY(cudaGetLastError());
+    SVD_CUDA_TRY(cudaDeviceSynchronize());
+    return SVDPHAT_OK;
+}
+
+namespace {
+struct DevBuf {
+    void* ptr = nullptr;
+    ~DevBuf() {
+        if (ptr) cudaFree(ptr);
+    }
+};
+}  // namespace
+
+svdphat_status setup_svd_operands(Plan& p, const double* d_tau_cls, int rank_D) {
+    const int n = p.Q_eff;
+    DevBuf G, lam, cnt, work, info, B, Wc, Vc;
+    SVD_CUDA_TRY(cudaMalloc(&G.ptr, (size_t)n * n * sizeof(cuDoubleComplex)));
+    SVD_CUDA_TRY(cudaMalloc(&lam.ptr, (size_t)n * sizeof(double)));
+    SVD_CUDA_TRY(cudaMalloc(&cnt.ptr, (size_t)n * sizeof(int)));
+    SVD_CUDA_TRY(cudaMalloc(&info.ptr, sizeof(int)));
+    SVD_CUDA_TRY(cudaMemcpy(cnt.ptr, p.cls_count.data(), (size_t)n * sizeof(int), cudaMemcpyHostToDevice));
+    {
+        dim3 grid(cdiv(n, 128), n);
+        gram_kernel<<<grid, 128>>>(d_tau_cls, (const int*)cnt.ptr, n, p.P, p.N, p.Kb, (cuDoubleComplex*)G.ptr);
+        SVD_CUDA_TRY(cudaGetLastError());
+    }
+    // ---- Hermitian eigendecomposition (float64, cuSOLVER)
+    cusolverDnHandle_t sh = nullptr;
+    if (cusolverDnCreate(&sh) != CUSOLVER_STATUS_SUCCESS) {
+        set_error("cusolverDnCreate failed");
+        return SVDPHAT_CUDA;
+    }
+    int lwork = 0;
+    cusolverStatus_t cs = cusolverDnZheevd_bufferSize(sh, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
+                                                      (cuDoubleComplex*)G.ptr, n, (double*)lam.ptr, &lwork);
+    if (cs != CUSOLVER_STATUS_SUCCESS) {
+        cusolverDnDestroy(sh);
+        set_error("cusolverDnZheevd_bufferSize failed: " + std::to_string((int)cs));
+        return SVDPHAT_CUDA;
+    }
+    {
+        cudaError_t e = cudaMalloc(&work.ptr, (size_t)lwork * sizeof(cuDoubleComplex));
+        if (e != cudaSuccess) {
+            cusolverDnDestroy(sh);
+            set_error("eigensolver workspace allocation failed");
+            return SVDPHAT_ALLOC;
+        }
+    }
+    cs = cusolverDnZheevd(sh, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, (cuDoubleComplex*)G.ptr, n,
+                          (double*)lam.ptr, (cuDoubleComplex*)work.ptr, lwork, (int*)info.ptr);
+    cudaError_t se = cudaDeviceSynchronize();
+    cusolverDnDestroy(sh);
+    int hinfo = 0;
+    cudaMemcpy(&hinfo, info.ptr, sizeof(int), cudaMemcpyDeviceToHost);
+    if (cs != CUSOLVER_STATUS_SUCCESS || se != cudaSuccess || hinfo != 0) {
+        set_error("cusolverDnZheevd failed: status " + std::to_string((int)cs) + " info " + std::to_string(hinfo));
+        return SVDPHAT_NUMERIC;
+    }
+    cudaFree(work.ptr);
+    work.ptr = nullptr;
+    std::vector<double> hl(n);
+    SVD_CUDA_TRY(cudaMemcpy(hl.data(), lam.ptr, (size_t)n * sizeof(double), cudaMemcpyDeviceToHost));
+    p.sigma2.resize(n);
+    for (int i = 0; i < n; ++i) p.sigma2[i] = std::max(0.0, hl[n - 1 - i]);
+    for (double v : p.sigma2)
+        if (!std::isfinite(v)) {
+            set_error("non-finite eigenvalue");
+            return SVDPHAT_NUMERIC;
+        }
+    // ---- rank rule (eq. 11): smallest D with sum_{d<=D} sigma^2 >= (1 - delta) Q P Kb
+    int numrank = 0;
+    for (int i = 0; i < n; ++i)
+        if (p.sigma2[i] > 1e-12 * p.sigma2[0]) numrank = i + 1;
+    int D = 0;
+    if (rank_D > 0) {
+        D = std::min(rank_D, numrank);
+    } else {
+        double acc = 0.0;
+        D = numrank;
+        for (int i = 0; i < n; ++i) {
+            acc += p.sigma2[i];
+            if (acc >= (1.0 - p.delta) * p.trace) {
+                D = i + 1;
+                break;
+            }
+        }
+        D = std::min(D, numrank);
+    }
+    if (D < 1) D = 1;
+    p.D = D;
+    double kept = 0.0;
+    for (int i = 0; i < D; ++i) kept += p.sigma2[i];
+    p.energy_kept = kept / p.trace;
+    p.Dh = (D + 63) / 64 * 64;
+    p.K2 = 3 * 2 * p.Dh;
+
+    // ---- V_D = W^H N^1/2 U' Lambda^{-1/2}, column chunks of W, ZGEMM (float64)
+    SVD_CUDA_TRY(cudaMalloc(&B.ptr, (size_t)n * D * sizeof(cuDoubleComplex)));
+    {
+        dim3 grid(cdiv(n, 128), D);
+        bmat_kernel<<<grid, 128>>>((const cuDoubleComplex*)G.ptr, (const double*)lam.ptr, (const int*)cnt.ptr, n, D,
+                                   (cuDoubleComplex*)B.ptr);
+        SVD_CUDA_TRY(cudaGetLastError());
+    }
+    p.bytes_V = (int64_t)2 * p.Dh * p.L.K_total * 2;
+    SVD_CUDA_TRY(cudaMalloc(&p.d_V16, p.bytes_V));
+    SVD_CUDA_TRY(cudaMemset(p.d_V16, 0, p.bytes_V));
+    int64_t CH = std::max<int64_t>(256, std::min<int64_t>(p.PK, (int64_t)(1ll << 30) / ((int64_t)n * 16)));
+    CH = std::min<int64_t>(CH, 16384);
+    SVD_CUDA_TRY(cudaMalloc(&Wc.ptr, (size_t)n * CH * sizeof(cuDoubleComplex)));
+    SVD_CUDA_TRY(cudaMalloc(&Vc.ptr, (size_t)CH * D * sizeof(cuDoubleComplex)));
+    cublasHandle_t bh = nullptr;
+    if (cublasCreate(&bh) != CUBLAS_STATUS_SUCCESS) {
+        set_error("cublasCreate failed");
+        return SVDPHAT_CUDA;
+    }
+    const cuDoubleComplex one = make_cuDoubleComplex(1, 0), zero = make_cuDoubleComplex(0, 0);
+    const double scale = std::sqrt((double)p.PK);
+    for (int64_t c0 = 0; c0 < p.PK; c0 += CH) {
+        const int C = (int)std::min<int64_t>(CH, p.PK - c0);
+        dim3 g1(cdiv(n, 128), C);
+        wchunk_kernel<<<g1, 128>>>(d_tau_cls, n, p.P, p.N, p.Kb, c0, C, (cuDoubleComplex*)Wc.ptr);
+        cublasStatus_t bs = cublasZgemm(bh, CUBLAS_OP_C, CUBLAS_OP_N, C, D, n, &one, (cuDoubleComplex*)Wc.ptr, n,
+                                        (cuDoubleComplex*)B.ptr, n, &zero, (cuDoubleComplex*)Vc.ptr, C);
+        if (bs != CUBLAS_STATUS_SUCCESS) {
+            cublasDestroy(bh);
+            set_error("cublasZgemm failed: " + std::to_string((int)bs));
+            return SVDPHAT_CUDA;
+        }
+        dim3 g2(cdiv(C, 128), D);
+        pack_v16_kernel<<<g2, 128>>>((const cuDoubleComplex*)Vc.ptr, C, D, p.Dh, c0, p.M, p.L.Mi, p.Kb, p.L.bpc,
+                                     p.L.U, p.L.K_total, scale, p.d_V16);
+    }
+    cublasDestroy(bh);
+    SVD_CUDA_TRY(cudaGetLastError());
+    // ---- normalised dictionary rows (split FP16)
+    p.bytes_R = (int64_t)p.Q_pad * p.K2 * 2;
+    SVD_CUDA_TRY(cudaMalloc(&p.d_R16, p.bytes_R));
+    SVD_CUDA_TRY(cudaMemset(p.d_R16, 0, p.bytes_R));
+    pack_r16_kernel<<<n, 256>>>((const cuDoubleComplex*)G.ptr, (const double*)lam.ptr, n, D, p.Dh, p.K2, p.d_R16);
+    SVD_CUDA_TRY(cudaGetLastError());
+    SVD_CUDA_TRY(cudaDeviceSynchronize());
+    return SVDPHAT_OK;
+}
+
+}  // namespace svdphat

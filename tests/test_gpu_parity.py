@@ -1,0 +1,185 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the float64 oracle on the same seeded inputs.
+
+Sizes: full frame sets for cfg1/cfg2 and a few cfg5 calls; cfg3/cfg4 at their full sizes with the oracle on a
+sampled subset of frames (the oracle computes them one by one).  Edge cases: empty batch, ragged tails, silent
+channels / degenerate frames, duplicate candidate points (tie -> lowest index), max_frames boundary.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("needs a CUDA device", allow_module_level=True)
+
+import paper_1811_11785_b200 as S  # noqa: E402
+from oracle import srpphat as srp  # noqa: E402
+from oracle import svdphat as svd  # noqa: E402
+from workloads import make  # noqa: E402
+from tests import _parity as PP  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def _plan(w, methods=("srp", "svd"), max_frames=None, rank_D=0):
+    return S.Plan(w.mics, w.points, w.fs, w.c, w.N, w.hop, w.field, rank_D=rank_D, delta=w.delta,
+                  methods=methods, max_frames=max_frames or w.frames_per_call)
+
+
+def _run(plan, w, method, audio_dev, F, offset=0):
+    doa = torch.full((max(F, 1),), -7, dtype=torch.int32, device=DEV)
+    score = torch.full((max(F, 1),), np.nan, dtype=torch.float32, device=DEV)
+    plan.localize(method, audio_dev.data_ptr() + 4 * offset, F, w.channel_stride, w.frame_stride, doa, score,
+                  torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    return doa[:F].cpu().numpy(), score[:F].cpu().numpy()
+
+
+def _check_degenerate(q, s, x):
+    dg = srp.degenerate(x)
+    assert np.all(q[dg] == -1) and np.all(s[dg] == 0.0)
+    return ~dg
+
+
+@pytest.fixture(scope="module")
+def cfg1():
+    w = make(1)
+    plan = _plan(w)
+    audio = torch.from_numpy(w.audio).to(DEV)
+    tau = srp.tdoa(w.mics, w.points, w.fs, w.c, w.field)
+    fr, x = PP.oracle_inputs(w)
+    fac = svd.svd_factors(tau, w.N, w.delta)
+    yield w, plan, audio, tau, fr, x, fac
+    plan.close()
+
+
+def test_phasors_match_oracle(cfg1):
+    w, plan, audio, tau, fr, x, fac = cfg1
+    _run(plan, w, "srp", audio, w.n_frames)
+    e_gpu = plan.debug_dump(S.DUMP_PHASORS, w.n_frames)
+    e_ref = srp.phat_phasors(srp.stft(fr))
+    err = np.abs((e_gpu[..., 0] + 1j * e_gpu[..., 1]) - e_ref)
+    assert err.max() < 3e-3, err.max()                 # FP16 phasors: |dphase| ~ 2^-11
+
+
+def test_class_representatives(cfg1):
+    w, plan, *_ = cfg1
+    rep = plan.debug_dump(S.DUMP_CLASS_REP, 0)
+    # planar array (z = 0): eq. 2 cannot tell u from its z-mirror, and nothing else -> classes = mirror pairs
+    g = w.points
+    idx = {tuple(p): i for i, p in enumerate(g)}
+    mirror = np.array([idx[tuple(p * [1.0, 1.0, -1.0])] for p in g])
+    expect = sorted(set(np.minimum(np.arange(len(g)), mirror).tolist()))
+    assert sorted(rep.tolist()) == expect
+    assert plan.info()["Q_classes"] == len(expect)
+
+
+def test_srp_cfg1_full(cfg1):
+    w, plan, audio, tau, fr, x, fac = cfg1
+    q, s = _run(plan, w, "srp", audio, w.n_frames)
+    keep = _check_degenerate(q, s, x)
+    Y, Y_at = PP.srp_reference(tau, x[keep], w.N)
+    st = PP.compare(q[keep], s[keep], Y, Y_at, "cfg1 SRP")
+    print(st)
+
+
+def test_svd_cfg1_full(cfg1):
+    w, plan, audio, tau, fr, x, fac = cfg1
+    assert plan.info()["D"] == fac["D"]
+    q, s = _run(plan, w, "svd", audio, w.n_frames)
+    keep = _check_degenerate(q, s, x)
+    Sv, Y_at = PP.svd_reference(fac, tau, x[keep], w.N)
+    st = PP.compare(q[keep], s[keep], Sv, Y_at, "cfg1 SVD")
+    print(st)
+
+
+def test_sigma2_matches_oracle(cfg1):
+    w, plan, audio, tau, fr, x, fac = cfg1
+    D = plan.info()["D"]
+    s2 = plan.sigma2(D + 5)
+    assert np.allclose(s2, fac["sigma2"][:D + 5], rtol=1e-9, atol=1e-9 * fac["sigma2"][0])
+
+
+def test_empty_and_ragged(cfg1):
+    w, plan, audio, *_ = cfg1
+    q0, s0 = _run(plan, w, "srp", audio, 0)
+    assert q0.size == 0
+    qa, sa = _run(plan, w, "srp", audio, w.n_frames)
+    for F in (1, 7, 33, 100):                            # ragged tails of the 256-frame tile
+        qb, sb = _run(plan, w, "srp", audio, F)
+        assert np.array_equal(qb, qa[:F]) and np.array_equal(sb, sa[:F])
+    # frames starting mid-stream (offset by 5 hops): same as frames 5.. of the full call
+    qc, sc = _run(plan, w, "srp", audio, 50, offset=5 * w.hop)
+    assert np.array_equal(qc, qa[5:55]) and np.array_equal(sc, sa[5:55])
+
+
+def test_invalid_arguments(cfg1):
+    w, plan, audio, *_ = cfg1
+    with pytest.raises(S.SvdPhatError):
+        _run(plan, w, "srp", audio, w.frames_per_call + 1)
+
+
+@pytest.mark.parametrize("cfg,frames", [(2, None), (5, 256 * 3)])
+def test_srp_svd_streams(cfg, frames):
+    w = make(cfg, frames)
+    plan = _plan(w, max_frames=min(w.n_frames, 4096) if cfg != 5 else 256)
+    audio = torch.from_numpy(w.audio).to(DEV)
+    tau = srp.tdoa(w.mics, w.points, w.fs, w.c, w.field)
+    fac = svd.svd_factors(tau, w.N, w.delta)
+    assert plan.info()["D"] == fac["D"]
+    per = w.frames_per_call if cfg == 5 else w.n_frames
+    rng = np.random.default_rng(cfg)
+    for c0 in range(0, w.n_frames, per):
+        F = min(per, w.n_frames - c0)
+        sub = np.arange(c0, c0 + F) if cfg == 5 else np.sort(rng.choice(w.n_frames, 400, replace=False))
+        fr = PP._frames_subset(w, sub)
+        x = srp.frames_to_x(fr)
+        for method in ("srp", "svd"):
+            q, s = _run(plan, w, method, audio, F, offset=c0 * w.frame_stride)
+            qs, ss = q[sub - c0], s[sub - c0]
+            keep = _check_degenerate(qs, ss, x)
+            if method == "srp":
+                P_, Y_at = PP.srp_reference(tau, x[keep], w.N)
+            else:
+                P_, Y_at = PP.svd_reference(fac, tau, x[keep], w.N)
+            print(cfg, method, PP.compare(qs[keep], ss[keep], P_, Y_at, f"cfg{cfg} {method} @{c0}"))
+    plan.close()
+
+
+def test_cfg3_full_batch_sampled():
+    w = make(3)
+    plan = _plan(w, methods=("srp",))
+    audio = torch.from_numpy(w.audio).to(DEV)
+    q, s = _run(plan, w, "srp", audio, w.n_frames)
+    rng = np.random.default_rng(3)
+    sub = np.sort(np.concatenate([rng.choice(w.n_frames, 46, replace=False), [0, w.n_frames - 1]]))
+    tau = srp.tdoa(w.mics, w.points, w.fs, w.c, w.field)
+    fr = PP._frames_subset(w, sub)
+    x = srp.frames_to_x(fr)
+    P_, Y_at = PP.srp_reference(tau, x, w.N)
+    print(PP.compare(q[sub], s[sub], P_, Y_at, "cfg3 SRP"))
+    # sanity vs truth: median angular error of the plane-wave direction
+    ang = np.degrees(np.arccos(np.clip(np.sum(w.points[q] * w.truth["u"], axis=1), -1, 1)))
+    assert np.median(ang) < 3.0
+    plan.close()
+
+
+def test_degenerate_and_duplicates():
+    w = make(1)
+    pts = np.concatenate([w.points[:100], w.points[:100]])     # exact duplicates: tie -> lowest index
+    plan = S.Plan(w.mics, pts, w.fs, w.c, w.N, w.hop, "far", methods=("srp", "svd"), max_frames=64)
+    a = w.audio[:, :20 * w.hop + w.N].copy()
+    a[:, :3 * w.hop + w.N] = 0.0                                  # frames 0..3 all-silent
+    a[1:, 5 * w.hop:8 * w.hop + w.N] = 0.0                        # frames 5..8: one live channel only
+    audio = torch.from_numpy(np.ascontiguousarray(a)).to(DEV)
+    F = S.frame_count(a.shape[1], w.N, w.hop)
+    for method in ("srp", "svd"):
+        doa = torch.zeros(F, dtype=torch.int32, device=DEV)
+        sc = torch.zeros(F, dtype=torch.float32, device=DEV)
+        plan.localize(method, audio, F, a.shape[1], w.hop, doa, sc, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        q = doa.cpu().numpy()
+        assert np.all(q[:4] == -1) and np.all(q[5:9] == -1), q
+        assert np.all((q[9:] >= 0) & (q[9:] < 100)), q
+    plan.close()
