@@ -34,7 +34,7 @@ typedef enum {
 } svdphat_status;
 
 enum { SVDPHAT_FIELD_FAR = 0, SVDPHAT_FIELD_NEAR = 1 };
-enum { SVDPHAT_METHOD_SRP = 1, SVDPHAT_METHOD_SVD = 2 };
+enum { SVDPHAT_METHOD_SRP = 1, SVDPHAT_METHOD_SVD = 2, SVDPHAT_METHOD_BOTH = 3 };
 
 typedef struct svdphat_plan_s* svdphat_plan_t;
 
@@ -95,6 +95,8 @@ svdphat_status svdphat_plan_sigma2(svdphat_plan_t plan, double* out, int32_t n);
  *   method   SVDPHAT_METHOD_SRP: eqs. 5-6 = Y = Re{W X} (eq. 9) + argmax;
  *            SVDPHAT_METHOD_SVD: Alg. 1 online: Z = V^H X (eq. 12), nearest normalised
  *            dictionary row (eqs. 14-15), then Y_q from the row of W.
+ *            SVDPHAT_METHOD_BOTH: both from one STFT pass; d_doa / d_score then hold 2*n_frames entries,
+ *            SRP results first, SVD results second.
  *   d_audio  DEVICE float32 samples: sample n of channel m in frame l is d_audio[m*channel_stride +
  *            l*frame_stride + n] (stream [M][L]: channel_stride=L, frame_stride=hop; framed [B][M][N]:
  *            channel_stride=N, frame_stride=M*N).  Must be 4-byte aligned.
@@ -108,7 +110,7 @@ svdphat_status svdphat_localize(svdphat_plan_t plan, int32_t method, const float
                                 void* stream);
 
 /* Same with HOST buffers: copies audio elements [0, audio_elems) host->device, localises, copies results back
- * and synchronises `stream`.  h_audio should be pinned for full bandwidth.  The device staging buffer is
+ * (2*n_frames entries for SVDPHAT_METHOD_BOTH) and synchronises `stream`.  h_audio should be pinned for full bandwidth.  The device staging buffer is
  * allocated on first use and kept by the plan (ALLOC on failure). */
 svdphat_status svdphat_localize_host(svdphat_plan_t plan, int32_t method, const float* h_audio,
                                      int64_t audio_elems, int64_t n_frames, int64_t channel_stride,
@@ -123,6 +125,22 @@ int64_t svdphat_frame_count(int64_t L, int32_t N, int32_t hop);
 
 const char* svdphat_status_str(svdphat_status s);
 const char* svdphat_last_error(void);
+
+/* ---- per-stage device timing (CUDA events recorded on the launching stream, for bench.py's roofline) ----
+ * After svdphat_profile_begin(plan, capacity), every localize records a start/end event pair around each of its
+ * kernels (up to `capacity` pairs).  svdphat_profile_end synchronises the events, writes up to `max` records
+ * (stage id, milliseconds) in launch order, returns the number written (negative status on error) and stops
+ * profiling.  Stage ids: */
+enum {
+    SVDPHAT_STAGE_STFT = 1,        /* sine-window STFT + PHAT phasors                                           */
+    SVDPHAT_STAGE_SRP_GEMM = 2,    /* Y = Re{W X} with fused cross-spectrum producer and argmax (eqs. 3, 5-9)   */
+    SVDPHAT_STAGE_SVD_PROJ = 3,    /* Z = V^H X with fused cross-spectrum producer (eq. 12)                     */
+    SVDPHAT_STAGE_SVD_NORM = 4,    /* Zhat = Z / ||Z||, split FP16                                              */
+    SVDPHAT_STAGE_SVD_SEARCH = 5,  /* Re{Dhat_q Zhat} + fused argmax (eqs. 14-15)                               */
+    SVDPHAT_STAGE_FINALIZE = 6     /* Y_q of the chosen q (eq. 5; Alg. 1 online step 4)                         */
+};
+svdphat_status svdphat_profile_begin(svdphat_plan_t plan, int32_t capacity);
+int32_t svdphat_profile_end(svdphat_plan_t plan, int32_t* stage_ids, float* ms, int32_t max);
 
 /* ---- test-only introspection (not part of the product path; used by tests/ for kernel-unit parity) ---- */
 enum {

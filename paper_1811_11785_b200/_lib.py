@@ -14,7 +14,9 @@ LIB_PATH = os.path.join(_HERE, "libsvdphat.so")
 
 OK, INVALID_ARG, ALLOC, CUDA, NUMERIC, UNSUPPORTED, TOO_LARGE = range(7)
 FIELD_FAR, FIELD_NEAR = 0, 1
-METHOD_SRP, METHOD_SVD = 1, 2
+METHOD_SRP, METHOD_SVD, METHOD_BOTH = 1, 2, 3
+STAGES = {1: "stft_phat", 2: "srp_gemm", 3: "svd_proj", 4: "svd_norm", 5: "svd_search", 6: "finalize"}
+_METHOD = {"srp": METHOD_SRP, "svd": METHOD_SVD, "both": METHOD_BOTH}
 DUMP_PHASORS, DUMP_Z, DUMP_CLASS_REP, DUMP_KEYS = 1, 2, 3, 4
 
 
@@ -35,7 +37,7 @@ class PlanInfo(C.Structure):
 
 def _load() -> C.CDLL:
     if not os.path.exists(LIB_PATH):
-        raise ImportError(f"{LIB_PATH} is missing: build it with `python -m paper_1811_11785_b200.build` "
+        raise ImportError(f"{LIB_PATH} is missing: build it with `python paper_1811_11785_b200/build.py` "
                           "(there is no CPU fallback)")
     lib = C.CDLL(LIB_PATH)
     vp, i32, i64, st = C.c_void_p, C.c_int32, C.c_int64, C.c_int
@@ -50,6 +52,8 @@ def _load() -> C.CDLL:
         "svdphat_status_str": (C.c_char_p, [st]),
         "svdphat_last_error": (C.c_char_p, []),
         "svdphat_debug_dump": (st, [vp, i32, i64, vp, i64]),
+        "svdphat_profile_begin": (st, [vp, i32]),
+        "svdphat_profile_end": (i32, [vp, C.POINTER(i32), C.POINTER(C.c_float), i32]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -116,17 +120,29 @@ class Plan:
 
     def localize(self, method: str, audio, n_frames: int, channel_stride: int, frame_stride: int, doa, score,
                  stream: int = 0) -> None:
-        """Device path: audio/doa/score are CUDA tensors (float32 / int32 / float32); async on `stream`."""
-        _check(lib.svdphat_localize(self._h, METHOD_SRP if method == "srp" else METHOD_SVD, _ptr(audio), n_frames,
+        """Device path: audio/doa/score are CUDA tensors (float32 / int32 / float32); async on `stream`.
+        method "srp" | "svd" | "both" (doa/score then hold 2*n_frames: SRP first, SVD second)."""
+        _check(lib.svdphat_localize(self._h, _METHOD[method], _ptr(audio), n_frames,
                                     channel_stride, frame_stride, _ptr(doa), _ptr(score), stream),
                "svdphat_localize")
 
     def localize_host(self, method: str, audio, audio_elems: int, n_frames: int, channel_stride: int,
                       frame_stride: int, doa, score, stream: int = 0) -> None:
         """Host path: audio/doa/score are host buffers (pinned for full bandwidth); synchronous."""
-        _check(lib.svdphat_localize_host(self._h, METHOD_SRP if method == "srp" else METHOD_SVD, _ptr(audio),
+        _check(lib.svdphat_localize_host(self._h, _METHOD[method], _ptr(audio),
                                          audio_elems, n_frames, channel_stride, frame_stride, _ptr(doa), _ptr(score),
                                          stream), "svdphat_localize_host")
+
+    def profile_begin(self, capacity: int) -> None:
+        _check(lib.svdphat_profile_begin(self._h, capacity), "profile_begin")
+
+    def profile_end(self, max_records: int = 1 << 16) -> list[tuple[str, float]]:
+        ids = (C.c_int32 * max_records)()
+        ms = (C.c_float * max_records)()
+        n = lib.svdphat_profile_end(self._h, ids, ms, max_records)
+        if n < 0:
+            raise SvdPhatError(-n, "profile_end")
+        return [(STAGES[ids[i]], float(ms[i])) for i in range(n)]
 
     def debug_dump(self, what: int, n_frames: int) -> np.ndarray:
         inf = self.info()

@@ -1,6 +1,6 @@
 """Build libsvdphat.so in-tree: nvcc for sm_100a (-gencode arch=compute_100a,code=sm_100a), -lineinfo, O3.
 
-Usage: python -m paper_1811_11785_b200.build [--force] [--verbose]
+Usage: python paper_1811_11785_b200/build.py [--force] [--verbose]   (does not import the package)
 Writes paper_1811_11785_b200/libsvdphat.so and build/ptxas.log (registers / spills per kernel).
 """
 from __future__ import annotations

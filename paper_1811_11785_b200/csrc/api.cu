@@ -102,6 +102,19 @@ static svdphat_status validate(const svdphat_plan_desc* d) {
     return SVDPHAT_OK;
 }
 
+// Records a start/end event pair around one kernel launch when profiling is on.
+template <class Fn>
+cudaError_t staged(Plan& p, int stage, cudaStream_t s, Fn&& fn) {
+    const bool rec = p.prof_on && p.prof_n < p.prof_cap;
+    if (rec) cudaEventRecord(p.prof_ev[2 * p.prof_n], s);
+    cudaError_t e = fn();
+    if (rec) {
+        cudaEventRecord(p.prof_ev[2 * p.prof_n + 1], s);
+        p.prof_stage[p.prof_n++] = stage;
+    }
+    return e;
+}
+
 }  // namespace svdphat
 
 using namespace svdphat;
@@ -109,6 +122,7 @@ using namespace svdphat;
 struct svdphat_plan_s {
     Plan p;
     ~svdphat_plan_s() {
+        for (cudaEvent_t e : p.prof_ev) cudaEventDestroy(e);
         void* bufs[] = {p.d_W16, p.d_V16, p.d_R16, p.d_rep, p.d_delay, p.d_window, p.d_twN, p.d_P16,
                         p.d_keys, p.d_Z32, p.d_Zs16, p.d_zflag, p.d_stage, p.d_doa_stage, p.d_score_stage};
         for (void* b : bufs)
@@ -353,9 +367,9 @@ svdphat_status svdphat_localize(svdphat_plan_t plan, int32_t method, const float
                                 void* stream) {
     if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
     Plan& p = plan->p;
-    if (method != SVDPHAT_METHOD_SRP && method != SVDPHAT_METHOD_SVD)
-        return fail(SVDPHAT_INVALID_ARG, "method must be SRP or SVD");
-    if (!(p.methods & method)) return fail(SVDPHAT_INVALID_ARG, "method was not planned");
+    if (method < SVDPHAT_METHOD_SRP || method > SVDPHAT_METHOD_BOTH)
+        return fail(SVDPHAT_INVALID_ARG, "method must be SRP, SVD or BOTH");
+    if ((p.methods & method) != method) return fail(SVDPHAT_INVALID_ARG, "method was not planned");
     if (n_frames < 0 || n_frames > p.max_frames) return fail(SVDPHAT_INVALID_ARG, "n_frames out of [0, max_frames]");
     if (n_frames == 0) return SVDPHAT_OK;
     if (!d_audio || !d_doa || !d_score) return fail(SVDPHAT_INVALID_ARG, "NULL buffer");
@@ -364,19 +378,63 @@ svdphat_status svdphat_localize(svdphat_plan_t plan, int32_t method, const float
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int F = (int)n_frames;
     SVD_CUDA_TRY(cudaSetDevice(p.device));
-    SVD_CUDA_TRY(launch_stft_phat(p, d_audio, channel_stride, frame_stride, F, s));
-    SVD_CUDA_TRY(cudaMemsetAsync(p.d_keys, 0, (size_t)F * 8, s));
-    if (method == SVDPHAT_METHOD_SRP) {
-        SVD_CUDA_TRY(launch_gemm(p, 0, F, s));
-    } else {
-        SVD_CUDA_TRY(launch_gemm(p, 1, F, s));
-        SVD_CUDA_TRY(launch_zsplit(p, F, s));
-        SVD_CUDA_TRY(launch_gemm(p, 2, F, s));
+    SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_STFT, s,
+                        [&] { return launch_stft_phat(p, d_audio, channel_stride, frame_stride, F, s); }));
+    int32_t* doa = d_doa;
+    float* score = d_score;
+    if (method & SVDPHAT_METHOD_SRP) {
+        SVD_CUDA_TRY(cudaMemsetAsync(p.d_keys, 0, (size_t)F * 8, s));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_GEMM, s, [&] { return launch_gemm(p, 0, F, s); }));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_FINALIZE, s,
+                            [&] { return launch_finalize(p, SVDPHAT_METHOD_SRP, F, doa, score, s); }));
+        doa += F;
+        score += F;
     }
-    SVD_CUDA_TRY(launch_finalize(p, method, F, d_doa, d_score, s));
+    if (method & SVDPHAT_METHOD_SVD) {
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_PROJ, s, [&] { return launch_gemm(p, 1, F, s); }));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_NORM, s, [&] { return launch_zsplit(p, F, s); }));
+        SVD_CUDA_TRY(cudaMemsetAsync(p.d_keys, 0, (size_t)F * 8, s));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_SEARCH, s, [&] { return launch_gemm(p, 2, F, s); }));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_FINALIZE, s,
+                            [&] { return launch_finalize(p, SVDPHAT_METHOD_SVD, F, doa, score, s); }));
+    }
     p.last_frames = F;
     p.last_method = method;
     return SVDPHAT_OK;
+}
+
+svdphat_status svdphat_profile_begin(svdphat_plan_t plan, int32_t capacity) {
+    if (!plan || capacity < 0) return fail(SVDPHAT_INVALID_ARG, "bad argument");
+    Plan& p = plan->p;
+    SVD_CUDA_TRY(cudaSetDevice(p.device));
+    for (cudaEvent_t e : p.prof_ev) cudaEventDestroy(e);
+    p.prof_ev.assign(2 * (size_t)capacity, nullptr);
+    for (auto& e : p.prof_ev) SVD_CUDA_TRY(cudaEventCreate(&e));
+    p.prof_stage.assign(capacity, 0);
+    p.prof_cap = capacity;
+    p.prof_n = 0;
+    p.prof_on = true;
+    return SVDPHAT_OK;
+}
+
+int32_t svdphat_profile_end(svdphat_plan_t plan, int32_t* stage_ids, float* ms, int32_t max) {
+    if (!plan) return -(int32_t)fail(SVDPHAT_INVALID_ARG, "plan is NULL");
+    Plan& p = plan->p;
+    cudaSetDevice(p.device);
+    int n = std::min(p.prof_n, std::max(0, max));
+    for (int i = 0; i < n; ++i) {
+        if (cudaEventSynchronize(p.prof_ev[2 * i + 1]) != cudaSuccess) return -(int32_t)SVDPHAT_CUDA;
+        float t = 0.f;
+        cudaEventElapsedTime(&t, p.prof_ev[2 * i], p.prof_ev[2 * i + 1]);
+        if (stage_ids) stage_ids[i] = p.prof_stage[i];
+        if (ms) ms[i] = t;
+    }
+    for (cudaEvent_t e : p.prof_ev) cudaEventDestroy(e);
+    p.prof_ev.clear();
+    p.prof_stage.clear();
+    p.prof_on = false;
+    p.prof_cap = p.prof_n = 0;
+    return n;
 }
 
 svdphat_status svdphat_localize_host(svdphat_plan_t plan, int32_t method, const float* h_audio, int64_t audio_elems,
@@ -400,16 +458,17 @@ svdphat_status svdphat_localize_host(svdphat_plan_t plan, int32_t method, const 
         p.stage_elems = audio_elems;
     }
     if (!p.d_doa_stage) {
-        if (cudaMalloc(&p.d_doa_stage, p.F_pad * sizeof(int32_t)) != cudaSuccess ||
-            cudaMalloc(&p.d_score_stage, p.F_pad * sizeof(float)) != cudaSuccess)
+        if (cudaMalloc(&p.d_doa_stage, 2 * p.F_pad * sizeof(int32_t)) != cudaSuccess ||
+            cudaMalloc(&p.d_score_stage, 2 * p.F_pad * sizeof(float)) != cudaSuccess)
             return fail(SVDPHAT_ALLOC, "result staging allocation failed");
     }
     SVD_CUDA_TRY(cudaMemcpyAsync(p.d_stage, h_audio, audio_elems * sizeof(float), cudaMemcpyHostToDevice, s));
     svdphat_status st = svdphat_localize(plan, method, p.d_stage, n_frames, channel_stride, frame_stride,
                                          p.d_doa_stage, p.d_score_stage, stream);
     if (st != SVDPHAT_OK) return st;
-    SVD_CUDA_TRY(cudaMemcpyAsync(h_doa, p.d_doa_stage, n_frames * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
-    SVD_CUDA_TRY(cudaMemcpyAsync(h_score, p.d_score_stage, n_frames * sizeof(float), cudaMemcpyDeviceToHost, s));
+    const int64_t nout = (method == SVDPHAT_METHOD_BOTH ? 2 : 1) * n_frames;
+    SVD_CUDA_TRY(cudaMemcpyAsync(h_doa, p.d_doa_stage, nout * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
+    SVD_CUDA_TRY(cudaMemcpyAsync(h_score, p.d_score_stage, nout * sizeof(float), cudaMemcpyDeviceToHost, s));
     SVD_CUDA_TRY(cudaStreamSynchronize(s));
     return SVDPHAT_OK;
 }

@@ -73,6 +73,11 @@ struct Plan {
     float* d_score_stage = nullptr;
     int64_t last_frames = 0;
     int last_method = 0;
+    // per-stage profiling
+    bool prof_on = false;
+    int prof_cap = 0, prof_n = 0;
+    std::vector<cudaEvent_t> prof_ev;   // 2 * prof_cap
+    std::vector<int> prof_stage;
 };
 
 // ---------------------------------------------------------------- error plumbing
