@@ -256,7 +256,11 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
         }
     }
     p.Q_eff = (int)p.rep_q.size();
-    p.Q_pad = (p.Q_eff + 127) / 128 * 128;
+    {
+        const char* e = getenv("SVDPHAT_PAIR_SRP");
+        p.pair_srp = e ? atoi(e) != 0 : true;
+    }
+    p.Q_pad = p.pair_srp ? (p.Q_eff + 255) / 256 * 256 : (p.Q_eff + 127) / 128 * 128;
 
     // ---- device tables
     std::vector<double> tau_cls((size_t)p.Q_eff * P);
@@ -311,13 +315,13 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     SVD_CUDA_TRY(cudaMalloc(&p.d_keys, Fp * sizeof(unsigned long long)));
     p.bytes_ws = bytes_P16 + Fp * 8;
     if (p.methods & SVDPHAT_METHOD_SVD) {
-        SVD_CUDA_TRY(cudaMalloc(&p.d_Z32, Fp * 2 * p.Dh * sizeof(float)));
-        SVD_CUDA_TRY(cudaMemset(p.d_Z32, 0, Fp * 2 * p.Dh * sizeof(float)));
+        SVD_CUDA_TRY(cudaMalloc(&p.d_Z32, MAX_KSPLIT * Fp * 2 * p.Dh * sizeof(float)));
+        SVD_CUDA_TRY(cudaMemset(p.d_Z32, 0, MAX_KSPLIT * Fp * 2 * p.Dh * sizeof(float)));
         SVD_CUDA_TRY(cudaMalloc(&p.d_Zs16, Fp * p.K2 * 2));
         SVD_CUDA_TRY(cudaMemset(p.d_Zs16, 0, Fp * p.K2 * 2));
         SVD_CUDA_TRY(cudaMalloc(&p.d_zflag, Fp * sizeof(int)));
         SVD_CUDA_TRY(cudaMemset(p.d_zflag, 0, Fp * sizeof(int)));
-        p.bytes_ws += Fp * 2 * p.Dh * 4 + Fp * p.K2 * 2 + Fp * 4;
+        p.bytes_ws += MAX_KSPLIT * Fp * 2 * p.Dh * 4 + Fp * p.K2 * 2 + Fp * 4;
         if (!encode_2d(&p.tm_Zs, p.d_Zs16, Fp, p.K2, 256))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(Zs) failed");
     }

@@ -13,12 +13,21 @@
 
 namespace svdphat {
 
-__global__ void zsplit_kernel(const float* __restrict__ Z, int F, int ldz, __half* __restrict__ Zs, int K2,
-                              int* __restrict__ zflag) {
+// Z = sum of the nsplit partial projections (fixed order: deterministic), then normalise and split.
+__global__ void zsplit_kernel(float* __restrict__ Z, int F, int64_t F_pad, int ldz, int nsplit,
+                              __half* __restrict__ Zs, int K2, int* __restrict__ zflag) {
     const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (warp >= F) return;
-    const float* z = Z + (int64_t)warp * ldz;
+    float* z = Z + (int64_t)warp * ldz;
+    if (nsplit > 1) {
+        for (int i = lane; i < ldz; i += 32) {
+            float v = z[i];
+            for (int s = 1; s < nsplit; ++s) v += z[(int64_t)s * F_pad * ldz + i];
+            z[i] = v;
+        }
+        __syncwarp();
+    }
     float ss = 0.f;
     for (int i = lane; i < ldz; i += 32) ss += z[i] * z[i];
 #pragma unroll
@@ -36,55 +45,90 @@ __global__ void zsplit_kernel(const float* __restrict__ Z, int F, int ldz, __hal
     }
 }
 
-__global__ void finalize_kernel(const unsigned long long* __restrict__ keys, const uint8_t* __restrict__ P16, int F,
-                                int64_t F_pad, int M, int Mi, int bpc, int n_chunks, int Kb, int N,
-                                const int* __restrict__ rep, const float* __restrict__ delay,
-                                const int* __restrict__ zflag, int32_t* __restrict__ doa, float* __restrict__ score) {
-    const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (f >= F) return;
-    const unsigned long long key = keys[f];
+// CTA = 32 consecutive frames (lane = frame, so every phasor record load is a coalesced 512-byte row) x 8 warps
+// striding over the bin chunks; partial sums meet in shared memory.
+constexpr int FIN_WARPS = 8;
+__global__ void __launch_bounds__(32 * FIN_WARPS)
+    finalize_kernel(const unsigned long long* __restrict__ keys, const uint8_t* __restrict__ P16, int F,
+                    int64_t F_pad, int M, int Mi, int bpc, int n_chunks, int Kb, int N,
+                    const int* __restrict__ rep, const float* __restrict__ delay, const int* __restrict__ zflag,
+                    int32_t* __restrict__ doa, float* __restrict__ score) {
+    __shared__ float s_y[FIN_WARPS][32];
+    __shared__ int s_p[FIN_WARPS][32];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int f = blockIdx.x * 32 + lane;
+    const bool valid = f < F;
+    const unsigned long long key = valid ? keys[f] : 0ull;
     const int cls = key ? (int)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull)) : -1;
     const int q = cls >= 0 ? rep[cls] : -1;
     const float* dq = delay + (int64_t)(q >= 0 ? q : 0) * M;
     const int ub = bpc * 4;
+    const float inv2N = 2.0f / (float)N;
     float ysum = 0.f;
     int pairs = 0;
-    for (int cc = lane; cc < n_chunks; cc += 32) {
-        float ar[4] = {0, 0, 0, 0}, ai[4] = {0, 0, 0, 0};
-        int nk[4] = {0, 0, 0, 0};
-        for (int m = 0; m < M; ++m) {
-            const float dlm = __ldg(dq + m);
-            const __half* rec =
-                reinterpret_cast<const __half*>(P16 + (((int64_t)cc * Mi + m) * F_pad + f) * ub);
-            for (int s = 0; s < bpc; ++s) {
-                const float er = __half2float(rec[s]), ei = __half2float(rec[bpc + s]);
-                if (er != 0.f || ei != 0.f) {
-                    const int k = cc * bpc + s;
-                    float sn, cs;
-                    sincospif(2.0f * (float)k * dlm / (float)N, &sn, &cs);
-                    ar[s] += er * cs - ei * sn;
-                    ai[s] += er * sn + ei * cs;
-                    nk[s] += 1;
+    if (valid) {
+        for (int cc = warp; cc < n_chunks; cc += FIN_WARPS) {
+            float ar[4] = {0, 0, 0, 0}, ai[4] = {0, 0, 0, 0};
+            int nk[4] = {0, 0, 0, 0};
+            const int kb0 = cc * bpc;
+            for (int m = 0; m < M; ++m) {
+                const float dl = __ldg(dq + m);
+                const uint8_t* rec = P16 + (((int64_t)cc * Mi + m) * F_pad + f) * ub;
+                float er[4], ei[4];
+                if (bpc == 4) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(rec));
+                    const float2 r01 = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
+                    const float2 r23 = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
+                    const float2 i01 = __half22float2(*reinterpret_cast<const __half2*>(&v.z));
+                    const float2 i23 = __half22float2(*reinterpret_cast<const __half2*>(&v.w));
+                    er[0] = r01.x; er[1] = r01.y; er[2] = r23.x; er[3] = r23.y;
+                    ei[0] = i01.x; ei[1] = i01.y; ei[2] = i23.x; ei[3] = i23.y;
+                } else {
+                    const uint2 v = __ldg(reinterpret_cast<const uint2*>(rec));
+                    const float2 r01 = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
+                    const float2 i01 = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
+                    er[0] = r01.x; er[1] = r01.y; ei[0] = i01.x; ei[1] = i01.y;
+                    er[2] = er[3] = ei[2] = ei[3] = 0.f;
+                }
+                // e^{+j 2 pi k delta_m / N} for k = kb0 .. kb0+bpc-1: base rotation, then unit steps
+                float bs, bc, ss, sc;
+                sincospif((float)kb0 * dl * inv2N, &bs, &bc);
+                sincospif(dl * inv2N, &ss, &sc);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+                    if (t < bpc && (er[t] != 0.f || ei[t] != 0.f)) {
+                        ar[t] += er[t] * bc - ei[t] * bs;
+                        ai[t] += er[t] * bs + ei[t] * bc;
+                        nk[t] += 1;
+                    }
+                    const float nb = bc * sc - bs * ss;
+                    bs = bs * sc + bc * ss;
+                    bc = nb;
+                }
+            }
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                if (t < bpc && kb0 + t < Kb) {
+                    ysum += ar[t] * ar[t] + ai[t] * ai[t] - (float)nk[t];
+                    pairs += nk[t] * (nk[t] - 1) / 2;
                 }
             }
         }
-        for (int s = 0; s < bpc; ++s) {
-            if (cc * bpc + s < Kb) {
-                ysum += ar[s] * ar[s] + ai[s] * ai[s] - (float)nk[s];
-                pairs += nk[s] * (nk[s] - 1) / 2;
-            }
-        }
     }
+    s_y[warp][lane] = ysum;
+    s_p[warp][lane] = pairs;
+    __syncthreads();
+    if (warp == 0 && valid) {
+        float y = 0.f;
+        int pr = 0;
 #pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) {
-        ysum += __shfl_xor_sync(0xffffffffu, ysum, o);
-        pairs += __shfl_xor_sync(0xffffffffu, pairs, o);
-    }
-    if (lane == 0) {
-        const bool dead = (pairs == 0) || q < 0 || (zflag != nullptr && zflag[f] != 0);
+        for (int w = 0; w < FIN_WARPS; ++w) {
+            y += s_y[w][lane];
+            pr += s_p[w][lane];
+        }
+        const bool dead = (pr == 0) || q < 0 || (zflag != nullptr && zflag[f] != 0);
         doa[f] = dead ? -1 : q;
-        score[f] = dead ? 0.f : 0.5f * ysum;
+        score[f] = dead ? 0.f : 0.5f * y;
     }
 }
 
@@ -92,15 +136,15 @@ cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s) {
     if (F <= 0) return cudaSuccess;
     const int threads = 256;
     const int blocks = (F * 32 + threads - 1) / threads;
-    zsplit_kernel<<<blocks, threads, 0, s>>>(p.d_Z32, F, 2 * p.Dh, p.d_Zs16, p.K2, p.d_zflag);
+    const int tiles = (2 * p.Dh / 128) * ((F + 255) / 256);
+    zsplit_kernel<<<blocks, threads, 0, s>>>(p.d_Z32, F, p.F_pad, 2 * p.Dh, ksplit_for(p, tiles), p.d_Zs16, p.K2,
+                                             p.d_zflag);
     return cudaGetLastError();
 }
 
 cudaError_t launch_finalize(const Plan& p, int method, int F, int32_t* doa, float* score, cudaStream_t s) {
     if (F <= 0) return cudaSuccess;
-    const int threads = 256;
-    const int blocks = (F * 32 + threads - 1) / threads;
-    finalize_kernel<<<blocks, threads, 0, s>>>(p.d_keys, p.d_P16, F, p.F_pad, p.M, p.L.Mi, p.L.bpc, p.L.n_chunks,
+    finalize_kernel<<<(F + 31) / 32, 32 * FIN_WARPS, 0, s>>>(p.d_keys, p.d_P16, F, p.F_pad, p.M, p.L.Mi, p.L.bpc, p.L.n_chunks,
                                                p.Kb, p.N, p.d_rep, p.d_delay,
                                                method == SVDPHAT_METHOD_SVD ? p.d_zflag : nullptr, doa, score);
     return cudaGetLastError();

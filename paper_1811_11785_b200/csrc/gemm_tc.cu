@@ -13,6 +13,8 @@
 // Warp roles: 0 TMA, 1 MMA issuer (one thread), 2..5 epilogue (TMEM lane groups 2,3,0,1), 6..13 producer.
 #include <cuda_fp16.h>
 
+#include <cstdlib>
+
 #include "internal.h"
 #include "ptx.cuh"
 
@@ -36,9 +38,36 @@ struct GemmParams {
     int m_tiles, n_tiles;
     int rows_valid;                        // rows of A that are real (mask for the argmax / store)
     unsigned long long* keys;              // argmax keys [F]
-    float* Z;                              // mode 1 output [F_pad][ldz]
+    float* Z;                              // mode 1 output [ksplit][F_pad][ldz] (partial sums per K split)
     int ldz;
+    int ksplit;                            // K splits (mode 1 only; splits fall on chunk boundaries)
+    int spc;                               // slabs per chunk
+    int prefetch;                          // 0 none, 1 L2 prefetch of the next chunk's phasors, 2 same evict_last
 };
+
+// Work unit t -> output tile (m, n) and the slab / chunk range of its K split.
+struct Unit {
+    int m, n, s, c0, c1, k0, k1;
+};
+__device__ __forceinline__ Unit unit_of(const GemmParams& p, int t) {
+    Unit u;
+    u.s = t % p.ksplit;
+    const int tile = t / p.ksplit;
+    u.m = tile / p.n_tiles;
+    u.n = tile % p.n_tiles;
+    if (p.ksplit == 1) {
+        u.c0 = 0;
+        u.c1 = p.n_chunks;
+        u.k0 = 0;
+        u.k1 = p.n_slabs;
+    } else {
+        u.c0 = (int)((int64_t)u.s * p.n_chunks / p.ksplit);
+        u.c1 = (int)((int64_t)(u.s + 1) * p.n_chunks / p.ksplit);
+        u.k0 = u.c0 * p.spc;
+        u.k1 = u.c1 * p.spc;
+    }
+    return u;
+}
 
 // ---------------------------------------------------------------- compile-time pair enumeration over Mi mics
 template <int Mi>
@@ -103,7 +132,7 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
 
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
-    const int n_tiles_total = p.m_tiles * p.n_tiles;
+    const int n_tiles_total = p.m_tiles * p.n_tiles * p.ksplit;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES; ++s) {
@@ -135,12 +164,12 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
             uint32_t phase = 0;
             const uint32_t bytes = kProducer ? A_BYTES : (A_BYTES + B_BYTES);
             for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
-                const int m = t / p.n_tiles, n = t % p.n_tiles;
-                for (int ks = 0; ks < p.n_slabs; ++ks) {
+                const Unit w = unit_of(p, t);
+                for (int ks = w.k0; ks < w.k1; ++ks) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     mbar_arrive_expect_tx(&full[stage], bytes);
-                    tma_load_2d(sA + stage * A_BYTES, &tmA, ks * BK, m * BM, &full[stage]);
-                    if (!kProducer) tma_load_2d(sB + stage * B_BYTES, &tmB, ks * BK, n * BN, &full[stage]);
+                    tma_load_2d(sA + stage * A_BYTES, &tmA, ks * BK, w.m * BM, &full[stage]);
+                    if (!kProducer) tma_load_2d(sB + stage * B_BYTES, &tmB, ks * BK, w.n * BN, &full[stage]);
                     if (++stage == STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -158,7 +187,8 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
             mbar_wait(&tempty[acc], acc_phase ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + acc * BN;
-            for (int ks = 0; ks < p.n_slabs; ++ks) {
+            const Unit w = unit_of(p, t);
+            for (int ks = w.k0; ks < w.k1; ++ks) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
                 if (lane == 0) {
@@ -167,7 +197,7 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
 #pragma unroll
                     for (int kk = 0; kk < BK / 16; ++kk) {
                         umma_f16(d_tmem, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), kIdesc,
-                                 (ks | kk) != 0);
+                                 (ks != w.k0) || (kk != 0));
                     }
                     umma_commit(&empty[stage]);
                 }
@@ -190,7 +220,9 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
-            const int m = t / p.n_tiles, n = t % p.n_tiles;
+            const Unit w = unit_of(p, t);
+            const int m = w.m, n = w.n;
+            float* Zs = p.Z + (int64_t)w.s * p.F_pad * p.ldz;
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int row = m * BM + g * 32 + lane;
@@ -205,7 +237,7 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
                     if (row_ok) {
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj) {
-                            if (f0 + jj < p.F) p.Z[(int64_t)(f0 + jj) * p.ldz + row] = __uint_as_float(r[jj]);
+                            if (f0 + jj < p.F) Zs[(int64_t)(f0 + jj) * p.ldz + row] = __uint_as_float(r[jj]);
                         }
                     }
                 } else {
@@ -237,11 +269,11 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
         uint32_t phase = 0;
         constexpr int kUB = BPC * 4;                               // bytes per phasor record: bpc*2 halves
         for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
-            const int n = t % p.n_tiles;
-            const int f = n * BN + tp;
+            const Unit w = unit_of(p, t);
+            const int f = w.n * BN + tp;
             const bool valid = f < p.F;
 #pragma unroll 1
-            for (int c = 0; c < p.n_chunks; ++c) {
+            for (int c = w.c0; c < w.c1; ++c) {
                 // e[m][w]: BPC=4 -> {Re k0k1, Re k2k3, Im k0k1, Im k2k3}; BPC=2 -> {Re k0k1, Im k0k1}
                 uint32_t e[Mi][BPC];
                 const uint8_t* src = p.P16 + ((int64_t)c * Mi * p.F_pad + f) * kUB;
@@ -259,6 +291,20 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
                                         : make_uint2(0, 0);
                         e[m][0] = v.x;
                         e[m][1] = v.y;
+                    }
+                }
+                // L2 prefetch of the next chunk's phasor records: the chunk-boundary reload then hits L2, well inside
+                // the STAGES-deep smem buffer (ncu r01: chunk-boundary HBM latency starved the MMA warp).
+                if (p.prefetch && valid && c + 1 < w.c1) {
+                    const uint8_t* nsrc = src + (int64_t)Mi * p.F_pad * kUB;
+                    if (p.prefetch == 2) {
+#pragma unroll
+                        for (int m = 0; m < Mi; ++m)
+                            asm volatile("prefetch.global.L2::evict_last [%0];" ::"l"(nsrc + (int64_t)m * p.F_pad * kUB));
+                    } else {
+#pragma unroll
+                        for (int m = 0; m < Mi; ++m)
+                            asm volatile("prefetch.global.L2 [%0];" ::"l"(nsrc + (int64_t)m * p.F_pad * kUB));
                     }
                 }
                 uint32_t outw[4];
@@ -315,6 +361,254 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
     }
 }
 
+// ================================================================================================================
+// CTA-pair variant (cta_group::2): one MMA computes a 256-row x 256-frame tile on two SMs.  CTA r of the pair
+// TMA-loads rows [m*256 + 128r, +128) of A and its 4 producer warps build frames [n*256 + 128r, +128) of B; the
+// even (leader) CTA issues tcgen05.mma.cta_group::2 for both.  Per SM this halves the shared-memory operand
+// traffic of the 1-CTA kernel (ncu r01: ~192 B/clk/SM needed at full MMA rate), the reason for the pair.
+// Warps: 0 TMA (+TMEM alloc), 1 MMA (leader), 2-3 idle, 4-7 epilogue (lane groups 0-3), 8-11 producer.
+// ================================================================================================================
+constexpr int STAGES2 = 6;
+constexpr int A2_BYTES = 128 * BK * 2;                 // 16 KB: this CTA's half of the 256 A rows
+constexpr int B2_BYTES = 128 * BK * 2;                 // 16 KB: this CTA's half of the 256 frames
+constexpr int NPW2 = 4;                                // producer warps per CTA (128 frames)
+constexpr int THREADS2 = 32 * (8 + NPW2);
+constexpr int SMEM2_BYTES = 1024 + STAGES2 * (A2_BYTES + B2_BYTES) + 256;
+
+template <int Mi, int BPC, int MODE>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
+    constexpr bool kProducer = (MODE != 2);
+    constexpr int kPairs = Mi * (Mi - 1) / 2;
+    constexpr int kUnitsRaw = (BPC == 4) ? kPairs : (kPairs + 1) / 2;
+    constexpr int kU = (kUnitsRaw + 7) / 8 * 8;
+    constexpr uint32_t kIdesc = umma_idesc_f16(256, 256);
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sA = smem;
+    uint8_t* sB = smem + STAGES2 * A2_BYTES;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES2 * B2_BYTES);
+    uint64_t* empty = full + STAGES2;
+    uint64_t* tfull = empty + STAGES2;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+    const int units = p.m_tiles * p.n_tiles * p.ksplit;   // m_tiles counts 256-row pair tiles
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES2; ++s) {
+            // leader: its TMA (expect_tx) + the producer warps of both CTAs (peer ones arrive remotely)
+            mbar_init(&full[s], kProducer ? 1 + 2 * NPW2 : 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 8);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc_2sm<512>(tmem_slot);
+    if (warp == 1 && lane == 0) {
+        tma_prefetch_desc(&tmA);
+        if (!kProducer) tma_prefetch_desc(&tmB);
+    }
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint32_t bytes = kProducer ? 2 * A2_BYTES : 2 * (A2_BYTES + B2_BYTES);
+            for (int t = pair; t < units; t += n_pairs) {
+                const Unit w = unit_of(p, t);
+                for (int ks = w.k0; ks < w.k1; ++ks) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
+                    tma_load_2d_2sm(sA + stage * A2_BYTES, &tmA, ks * BK, w.m * 256 + (int)rank * 128, &full[stage]);
+                    if (!kProducer)
+                        tma_load_2d_2sm(sB + stage * B2_BYTES, &tmB, ks * BK, w.n * BN + (int)rank * 128, &full[stage]);
+                    if (++stage == STAGES2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader) {
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = pair; t < units; t += n_pairs) {
+                const Unit w = unit_of(p, t);
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t d_tmem = tmem_base + acc * BN;
+                for (int ks = w.k0; ks < w.k1; ++ks) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t a0 = smem_u32(sA + stage * A2_BYTES);
+                        const uint32_t b0 = smem_u32(sB + stage * B2_BYTES);
+#pragma unroll
+                        for (int kk = 0; kk < BK / 16; ++kk)
+                            umma_f16_2sm(d_tmem, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), kIdesc,
+                                         (ks != w.k0) || (kk != 0));
+                        umma_commit_2sm(&empty[stage], 0x3);
+                    }
+                    __syncwarp();
+                    if (++stage == STAGES2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                if (lane == 0) umma_commit_2sm(&tfull[acc], 0x3);
+                __syncwarp();
+                if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp >= 4 && warp < 8) {
+        const int g = warp & 3;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = pair; t < units; t += n_pairs) {
+            const Unit w = unit_of(p, t);
+            float* Zs = p.Z + (int64_t)w.s * p.F_pad * p.ldz;
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int row = w.m * 256 + (int)rank * 128 + g * 32 + lane;
+            const bool row_ok = row < p.rows_valid;
+#pragma unroll 1
+            for (int j0 = 0; j0 < BN; j0 += 32) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + acc * BN + j0, r);
+                tmem_ld_wait();
+                const int f0 = w.n * BN + j0;
+                if (MODE == 1) {
+                    if (row_ok) {
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj)
+                            if (f0 + jj < p.F) Zs[(int64_t)(f0 + jj) * p.ldz + row] = __uint_as_float(r[jj]);
+                    }
+                } else {
+                    unsigned long long k[32];
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj) {
+                        const float v = __uint_as_float(r[jj]);
+                        k[jj] = row_ok ? make_key(v, (uint32_t)row) : 0ull;
+                    }
+                    const unsigned long long best = transpose_max32(k, lane);
+                    if (f0 + lane < p.F && best != 0ull) atomicMax(&p.keys[f0 + lane], best);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
+            if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    } else if (warp >= 8 && kProducer) {
+        constexpr PairTab<Mi> PT{};
+        const int tp = (warp - 8) * 32 + lane;                    // frame row of this CTA's half tile: 0..127
+        const uint32_t row_off = (uint32_t)((tp >> 3) * 1024 + (tp & 7) * 128);
+        const uint32_t xr = (uint32_t)(tp & 7);
+        int stage = 0;
+        uint32_t phase = 0;
+        constexpr int kUB = BPC * 4;
+        for (int t = pair; t < units; t += n_pairs) {
+            const Unit w = unit_of(p, t);
+            const int f = w.n * BN + (int)rank * 128 + tp;
+            const bool valid = f < p.F;
+#pragma unroll 1
+            for (int c = w.c0; c < w.c1; ++c) {
+                uint32_t e[Mi][BPC];
+                const uint8_t* src = p.P16 + ((int64_t)c * Mi * p.F_pad + f) * kUB;
+#pragma unroll
+                for (int m = 0; m < Mi; ++m) {
+                    if constexpr (BPC == 4) {
+                        uint4 v = valid ? __ldg(reinterpret_cast<const uint4*>(src + (int64_t)m * p.F_pad * kUB))
+                                        : make_uint4(0, 0, 0, 0);
+                        e[m][0] = v.x;
+                        e[m][1] = v.y;
+                        e[m][2] = v.z;
+                        e[m][3] = v.w;
+                    } else {
+                        uint2 v = valid ? __ldg(reinterpret_cast<const uint2*>(src + (int64_t)m * p.F_pad * kUB))
+                                        : make_uint2(0, 0);
+                        e[m][0] = v.x;
+                        e[m][1] = v.y;
+                    }
+                }
+                uint32_t outw[4];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    if ((u & 7) == 0) mbar_wait(&empty[stage], phase ^ 1);
+                    if constexpr (BPC == 4) {
+                        if (u < kPairs) {
+                            const int a = PT.i[u], b = PT.j[u];
+                            const uint32_t nra01 = e[a][0] ^ 0x80008000u, nra23 = e[a][1] ^ 0x80008000u;
+                            outw[0] = h2fma(e[a][0], e[b][0], h2mul(e[a][2], e[b][2]));
+                            outw[1] = h2fma(e[a][1], e[b][1], h2mul(e[a][3], e[b][3]));
+                            outw[2] = h2fma(e[a][2], e[b][0], h2mul(nra01, e[b][2]));
+                            outw[3] = h2fma(e[a][3], e[b][1], h2mul(nra23, e[b][3]));
+                        } else {
+                            outw[0] = outw[1] = outw[2] = outw[3] = 0u;
+                        }
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int pp = 2 * u + h;
+                            if (pp < kPairs) {
+                                const int a = PT.i[pp], b = PT.j[pp];
+                                const uint32_t nra = e[a][0] ^ 0x80008000u;
+                                outw[2 * h + 0] = h2fma(e[a][0], e[b][0], h2mul(e[a][1], e[b][1]));
+                                outw[2 * h + 1] = h2fma(e[a][1], e[b][0], h2mul(nra, e[b][1]));
+                            } else {
+                                outw[2 * h + 0] = outw[2 * h + 1] = 0u;
+                            }
+                        }
+                    }
+                    const uint32_t dst = smem_u32(sB + stage * B2_BYTES) + row_off + ((((uint32_t)u & 7u) ^ xr) << 4);
+                    st_shared_v4(dst, outw[0], outw[1], outw[2], outw[3]);
+                    if ((u & 7) == 7) {
+                        fence_proxy_async_smem();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(&full[stage], 0);   // the leader's barrier
+                        if (++stage == STAGES2) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc_2sm<512>(tmem_base);
+    }
+}
+
 // ---------------------------------------------------------------- host side
 template <int Mi, int BPC, int MODE>
 static cudaError_t set_attr_one() {
@@ -322,8 +616,18 @@ static cudaError_t set_attr_one() {
                                 SMEM_BYTES);
 }
 
+template <int Mi, int BPC, int MODE>
+static cudaError_t set_attr_two() {
+    return cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                SMEM2_BYTES);
+}
+
 cudaError_t gemm_set_attributes() {
     cudaError_t e = cudaSuccess;
+    if ((e = set_attr_two<4, 4, 0>()) != cudaSuccess) return e;
+    if ((e = set_attr_two<8, 4, 0>()) != cudaSuccess) return e;
+    if ((e = set_attr_two<16, 4, 0>()) != cudaSuccess) return e;
+    if ((e = set_attr_two<32, 2, 0>()) != cudaSuccess) return e;
 #define SVD_ATTR(MI, B)                                        \
     if ((e = set_attr_one<MI, B, 0>()) != cudaSuccess) return e; \
     if ((e = set_attr_one<MI, B, 1>()) != cudaSuccess) return e;
@@ -342,6 +646,20 @@ static cudaError_t launch_one(const CUtensorMap& A, const CUtensorMap& B, const 
     return cudaGetLastError();
 }
 
+int ksplit_for(const Plan& p, int tiles) {
+    int best = 1;
+    double best_t = 1e30;
+    for (int S = 1; S <= MAX_KSPLIT && S <= p.L.n_chunks; ++S) {
+        const double waves = (double)((tiles * S + p.num_sms - 1) / p.num_sms);
+        const double t = waves / S;
+        if (t < best_t - 1e-9) {
+            best_t = t;
+            best = S;
+        }
+    }
+    return best;
+}
+
 cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
     GemmParams gp{};
     gp.P16 = p.d_P16;
@@ -352,6 +670,13 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
     gp.keys = p.d_keys;
     gp.Z = p.d_Z32;
     gp.ldz = 2 * p.Dh;
+    gp.ksplit = 1;
+    gp.spc = p.L.U / 8;
+    static const int pf = [] {
+        const char* e = getenv("SVDPHAT_GEMM_PREFETCH");
+        return e ? atoi(e) : 1;
+    }();
+    gp.prefetch = pf;
     const CUtensorMap* A = nullptr;
     const CUtensorMap* B = &p.tm_W;  // unused placeholder for producer modes
     if (mode == 0) {
@@ -371,10 +696,31 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
         gp.m_tiles = p.Q_pad / BM;
         gp.rows_valid = p.Q_eff;
     }
-    const int tiles = gp.m_tiles * gp.n_tiles;
+    int tiles = gp.m_tiles * gp.n_tiles;
+    if (mode == 1) {
+        // split K (at chunk boundaries) to fill the SMs: minimise waves / split, deterministic partial buffers
+        gp.ksplit = ksplit_for(p, tiles);
+        tiles *= gp.ksplit;
+    }
     const int grid = tiles < p.num_sms ? tiles : p.num_sms;
     if (tiles == 0) return cudaSuccess;
     if (mode == 2) return launch_one<4, 4, 2>(*A, *B, gp, grid, s);
+    if (mode == 0 && p.pair_srp) {
+        gp.m_tiles = p.Q_pad / 256;
+        const int units = gp.m_tiles * gp.n_tiles;
+        const int pairs = units < p.num_sms / 2 ? units : p.num_sms / 2;
+#define SVD_DISPATCH2(MI, BP)                                                                                \
+    if (p.L.Mi == MI) {                                                                                     \
+        gemm2_kernel<MI, BP, 0><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(*A, *B, gp);                        \
+        return cudaGetLastError();                                                                          \
+    }
+        SVD_DISPATCH2(4, 4)
+        SVD_DISPATCH2(8, 4)
+        SVD_DISPATCH2(16, 4)
+        SVD_DISPATCH2(32, 2)
+#undef SVD_DISPATCH2
+        return cudaErrorInvalidValue;
+    }
 #define SVD_DISPATCH(MI, BP)                                                                      \
     if (p.L.Mi == MI) {                                                                          \
         return mode == 0 ? launch_one<MI, BP, 0>(*A, *B, gp, grid, s) : launch_one<MI, BP, 1>(*A, *B, gp, grid, s); \

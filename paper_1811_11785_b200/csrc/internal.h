@@ -56,7 +56,7 @@ struct Plan {
     // workspace
     uint8_t* d_P16 = nullptr;     // phasors
     unsigned long long* d_keys = nullptr;  // [F_pad]
-    float* d_Z32 = nullptr;       // [F_pad][2*Dh]
+    float* d_Z32 = nullptr;       // [MAX_KSPLIT][F_pad][2*Dh] partial Z of the split-K projection
     __half* d_Zs16 = nullptr;     // [F_pad][K2]
     int* d_zflag = nullptr;       // [F_pad]
     int64_t bytes_W = 0, bytes_V = 0, bytes_R = 0, bytes_ws = 0;
@@ -66,6 +66,7 @@ struct Plan {
     alignas(64) CUtensorMap tm_R;
     alignas(64) CUtensorMap tm_Zs;
     int num_sms = 148;
+    bool pair_srp = true;          // SRP GEMM on CTA pairs (cta_group::2); Q_pad is then a multiple of 256
     // host-buffer path
     float* d_stage = nullptr;
     int64_t stage_elems = 0;
@@ -99,6 +100,8 @@ cudaError_t launch_stft_phat(const Plan& p, const float* audio, int64_t cs, int6
 //       2 = SVD search argmax (A = R16, B = Zs16 via TMA)
 cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s);
 cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s);
+constexpr int MAX_KSPLIT = 4;
+int ksplit_for(const Plan& p, int tiles);   // K splits of the SVD projection GEMM for its tile count
 cudaError_t launch_finalize(const Plan& p, int method, int F, int32_t* doa, float* score, cudaStream_t s);
 cudaError_t gemm_set_attributes();
 

@@ -29,7 +29,35 @@ __device__ __forceinline__ float2 phat(float2 X) {
     return make_float2(0.f, 0.f);
 }
 
-template <int R>  // N = 64 R, N/2 = 32 R complex points
+// In-register radix-2 DIF DFT of R points (twiddles from the N-point table); output a[i] = DFT[bitrev_R(i)].
+template <int R>
+__device__ __forceinline__ void dft_dif(float2 (&a)[R], const float2* __restrict__ twN, int N) {
+#pragma unroll
+    for (int h = R / 2; h >= 1; h >>= 1) {
+#pragma unroll
+        for (int s0 = 0; s0 < R; s0 += 2 * h) {
+#pragma unroll
+            for (int t = 0; t < h; ++t) {
+                const float2 u = a[s0 + t], v = a[s0 + t + h];
+                a[s0 + t] = make_float2(u.x + v.x, u.y + v.y);
+                const float2 d = make_float2(u.x - v.x, u.y - v.y);
+                a[s0 + t + h] = (t == 0) ? d : cmul(d, __ldg(twN + t * (N / (2 * h))));
+            }
+        }
+    }
+}
+
+template <int R>
+__device__ __forceinline__ int bitrev_r(int i) {
+    int lg = 0;
+    while ((1 << lg) < R) ++lg;
+    return lg == 0 ? 0 : (int)(__brev((unsigned)i) >> (32 - lg));
+}
+
+// Complex H = 32R point FFT of z[n'] = x[2n'] + j x[2n'+1] as 32R = R x 32 (pass 1: R-point DFTs over r in
+// registers, twiddle, transpose through padded smem; pass 2: the 32-point DFTs over the lane index split as
+// R-point in registers x G = 32/R across lanes).  Then the real-FFT post pass, PHAT, FP16 records.
+template <int R>
 __global__ void __launch_bounds__(32 * STFT_WARPS)
     stft_phat_kernel(const float* __restrict__ audio, int64_t cs, int64_t fstride, int F, int Mi, int64_t F_pad,
                      const float* __restrict__ win, const float2* __restrict__ twN, uint8_t* __restrict__ P16,
@@ -37,19 +65,21 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
     constexpr int N = 64 * R;
     constexpr int H = N / 2;
     constexpr int Kb = H + 1;
+    constexpr int G = 32 / R;                     // lanes per 32-point DFT in pass 2 (R <= 32)
+    constexpr int SROW = 34;                      // padded row (float2) of the pass-1 transpose S[k1][l]
+    constexpr int WBUF = (R * SROW > H + H / 32 + 2) ? R * SROW : H + H / 32 + 2;   // float2 per warp
     extern __shared__ __align__(16) uint8_t sm[];
-    float2* zbuf = reinterpret_cast<float2*>(sm);                         // [8][H]
-    const int unit_bytes = bpc * 4;
-    uint8_t* tile = sm + STFT_WARPS * H * sizeof(float2);                 // [n_chunks][8][unit_bytes]
+    float2* wbuf = reinterpret_cast<float2*>(sm) + (threadIdx.x >> 5) * WBUF;
+    const int tile_stride = STFT_WARPS * 16 + 16;                                    // padded chunk row (bytes)
+    uint8_t* tile = sm + STFT_WARPS * WBUF * sizeof(float2);                        // [n_chunks][tile_stride]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m = blockIdx.y;
     const int f0 = blockIdx.x * STFT_WARPS;
     const int f = f0 + warp;
-    float2* z = zbuf + warp * H;
+    const bool live = f < F;
 
-    if (f < F) {
-        // ---- load + window: z[n'] for n' = lane + 32 r
+    if (live) {
         const float* x = audio + (int64_t)m * cs + (int64_t)f * fstride;
         float2 a[R];
 #pragma unroll
@@ -57,88 +87,80 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
             const int n2 = 2 * (lane + 32 * r);
             a[r] = make_float2(__ldg(x + n2) * __ldg(win + n2), __ldg(x + n2 + 1) * __ldg(win + n2 + 1));
         }
-        // ---- R-point DFT over r (radix-2 DIF, output index bit-reversed)
-#pragma unroll
-        for (int h = R / 2; h >= 1; h >>= 1) {
-#pragma unroll
-            for (int s0 = 0; s0 < R; s0 += 2 * h) {
-#pragma unroll
-                for (int t = 0; t < h; ++t) {
-                    const float2 u = a[s0 + t], v = a[s0 + t + h];
-                    a[s0 + t] = make_float2(u.x + v.x, u.y + v.y);
-                    a[s0 + t + h] = cmul(make_float2(u.x - v.x, u.y - v.y), __ldg(twN + t * (N / (2 * h))));
-                }
-            }
-        }
-        // ---- twiddle by W_{N/2}^{lane * k1} = e^{-j 2 pi 2 lane k1 / N}, then 32-point DIF across lanes
-        int logR = 0;
-        while ((1 << logR) < R) ++logR;
+        // pass 1: DFT over r, twiddle W_H^{lane k1}, transpose S[k1][lane]
+        dft_dif<R>(a, twN, N);
 #pragma unroll
         for (int i = 0; i < R; ++i) {
-            const int k1 = (R == 1) ? 0 : (int)(__brev((unsigned)i) >> (32 - logR));
-            a[i] = cmul(a[i], __ldg(twN + ((2 * lane * k1) % N)));
+            const int k1 = bitrev_r<R>(i);
+            wbuf[k1 * SROW + lane] = (k1 == 0) ? a[i] : cmul(a[i], __ldg(twN + ((2 * lane * k1) % N)));
+        }
+        __syncwarp();
+        // pass 2: lane (k1 = lane / G, h = lane % G) takes l = G j + h, j < R
+        const int k1 = lane / G, h = lane % G;
 #pragma unroll
-            for (int h = 16; h >= 1; h >>= 1) {
-                const float ox = __shfl_xor_sync(0xffffffffu, a[i].x, h);
-                const float oy = __shfl_xor_sync(0xffffffffu, a[i].y, h);
-                if (lane & h) {
-                    // (other - mine) * w_{2h}^{lane mod h}
-                    a[i] = cmul(make_float2(ox - a[i].x, oy - a[i].y), __ldg(twN + (lane & (h - 1)) * (N / (2 * h))));
+        for (int j = 0; j < R; ++j) a[j] = wbuf[k1 * SROW + G * j + h];
+        __syncwarp();
+        dft_dif<R>(a, twN, N);                                  // a[i] = E_h[bitrev(i)]
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int aa = bitrev_r<R>(i);
+            if (h * aa) a[i] = cmul(a[i], __ldg(twN + ((h * aa) * (N / 32)) % N));   // W_32^{h a}
+#pragma unroll
+            for (int hh = G / 2; hh >= 1; hh >>= 1) {           // G-point DIF across the lane group
+                const float ox = __shfl_xor_sync(0xffffffffu, a[i].x, hh);
+                const float oy = __shfl_xor_sync(0xffffffffu, a[i].y, hh);
+                if (h & hh) {
+                    const int tw = (h & (hh - 1)) * (N / (2 * hh));
+                    const float2 d = make_float2(ox - a[i].x, oy - a[i].y);
+                    a[i] = tw ? cmul(d, __ldg(twN + tw)) : d;
                 } else {
                     a[i] = make_float2(a[i].x + ox, a[i].y + oy);
                 }
             }
-            z[k1 + R * bitrev5(lane)] = a[i];
         }
+        // Z[k1 + R (a + R bitrev_G(h))] -> natural order, padded by one float2 per 32
+        int bg = 0;
+        {
+            int lg = 0;
+            while ((1 << lg) < G) ++lg;
+            bg = lg == 0 ? 0 : (int)(__brev((unsigned)h) >> (32 - lg));
+        }
+#pragma unroll
+        for (int i = 0; i < R; ++i) {
+            const int k = k1 + R * (bitrev_r<R>(i) + R * bg);
+            wbuf[k + (k >> 5)] = a[i];
+        }
+        __syncwarp();
     }
-    __syncwarp();
 
-    // ---- real-FFT post pass + PHAT + pack records into the CTA tile
-    for (int cc = lane; cc < n_chunks; cc += 32) {
-        uint32_t w[4] = {0u, 0u, 0u, 0u};
-        if (f < F) {
-            float re[4], im[4];
-            for (int s = 0; s < bpc; ++s) {
-                const int k = cc * bpc + s;
-                float2 e = make_float2(0.f, 0.f);
-                if (k < Kb) {
-                    const float2 Zk = z[k & (H - 1)];
-                    const float2 Zm = z[(H - k) & (H - 1)];
-                    const float2 Zr = make_float2(Zm.x, -Zm.y);                              // conj(Z[H-k])
-                    const float2 E = make_float2(0.5f * (Zk.x + Zr.x), 0.5f * (Zk.y + Zr.y));
-                    const float2 Dd = make_float2(0.5f * (Zk.x - Zr.x), 0.5f * (Zk.y - Zr.y));
-                    const float2 t = cmul(__ldg(twN + (k % N)), Dd);                        // w^k (Z - Zr)/2
-                    e = phat(make_float2(E.x + t.y, E.y - t.x));                            // E - j t
-                }
-                re[s] = e.x;
-                im[s] = e.y;
-            }
-            if (bpc == 4) {
-                __half2 h0 = __floats2half2_rn(re[0], re[1]), h1 = __floats2half2_rn(re[2], re[3]);
-                __half2 h2 = __floats2half2_rn(im[0], im[1]), h3 = __floats2half2_rn(im[2], im[3]);
-                w[0] = *reinterpret_cast<uint32_t*>(&h0);
-                w[1] = *reinterpret_cast<uint32_t*>(&h1);
-                w[2] = *reinterpret_cast<uint32_t*>(&h2);
-                w[3] = *reinterpret_cast<uint32_t*>(&h3);
-            } else {
-                __half2 h0 = __floats2half2_rn(re[0], re[1]), h1 = __floats2half2_rn(im[0], im[1]);
-                w[0] = *reinterpret_cast<uint32_t*>(&h0);
-                w[1] = *reinterpret_cast<uint32_t*>(&h1);
-            }
+    // ---- real-FFT post pass + PHAT per bin (lanes over consecutive bins), halves into the padded record tile
+    for (int k = lane; k < n_chunks * bpc; k += 32) {
+        float2 e = make_float2(0.f, 0.f);
+        if (live && k < Kb) {
+            const int k0 = k & (H - 1), km = (H - k) & (H - 1);
+            const float2 Zk = wbuf[k0 + (k0 >> 5)];
+            const float2 Zm = wbuf[km + (km >> 5)];
+            const float2 Zr = make_float2(Zm.x, -Zm.y);                                  // conj(Z[H-k])
+            const float2 E = make_float2(0.5f * (Zk.x + Zr.x), 0.5f * (Zk.y + Zr.y));
+            const float2 Dd = make_float2(0.5f * (Zk.x - Zr.x), 0.5f * (Zk.y - Zr.y));
+            const float2 t = cmul(__ldg(twN + k), Dd);                                   // w^k (Z - Zr)/2
+            e = phat(make_float2(E.x + t.y, E.y - t.x));                                // E - j t
         }
-        uint32_t* dst = reinterpret_cast<uint32_t*>(tile + ((int64_t)cc * STFT_WARPS + warp) * unit_bytes);
-        for (int q = 0; q < bpc; ++q) dst[q] = w[q];
+        const int cc = k / bpc, s = k % bpc;
+        __half* rec = reinterpret_cast<__half*>(tile + cc * tile_stride + warp * (bpc * 4));
+        rec[s] = __float2half_rn(e.x);
+        rec[bpc + s] = __float2half_rn(e.y);
     }
     __syncthreads();
 
     // ---- coalesced write-out: per chunk, 8 frames x unit_bytes contiguous at P16[c][m][f0..f0+7]
+    const int unit_bytes = bpc * 4;
     const int words_per_chunk = STFT_WARPS * unit_bytes / 4;
     const int total = n_chunks * words_per_chunk;
-    const uint32_t* t32 = reinterpret_cast<const uint32_t*>(tile);
     for (int i = threadIdx.x; i < total; i += blockDim.x) {
         const int cc = i / words_per_chunk, wi = i % words_per_chunk;
         uint32_t* out = reinterpret_cast<uint32_t*>(P16 + (((int64_t)cc * Mi + m) * F_pad + f0) * unit_bytes);
-        out[wi] = t32[i];
+        out[wi] = reinterpret_cast<const uint32_t*>(tile + cc * tile_stride)[wi];
     }
 }
 
@@ -190,7 +212,8 @@ __global__ void stft_phat_small_kernel(const float* __restrict__ audio, int64_t 
 template <int R>
 static cudaError_t launch_r(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F, cudaStream_t s) {
     const int H = 32 * R;
-    const size_t smem = STFT_WARPS * H * sizeof(float2) + (size_t)p.L.n_chunks * STFT_WARPS * p.L.unit_bytes;
+    const int wbuf = (R * 34 > H + H / 32 + 2) ? R * 34 : H + H / 32 + 2;
+    const size_t smem = STFT_WARPS * wbuf * sizeof(float2) + (size_t)p.L.n_chunks * (STFT_WARPS * 16 + 16);
     static bool attr_done = false;
     if (!attr_done) {
         cudaError_t e = cudaFuncSetAttribute(stft_phat_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
