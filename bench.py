@@ -121,6 +121,20 @@ def cpu_baseline(w, n_frames: int) -> dict:
             "seconds": dt}
 
 
+def aggregate(ms_local: float, frames_local: int, dist=None, device=None) -> tuple[float, float]:
+    """Weak scaling, no data-path collective: step time = MAX over ranks of each rank's device time; value = all
+    ranks' frames / that time.  Returns (ms_per_step, frames_per_second)."""
+    ms, fr = ms_local, float(frames_local)
+    if dist is not None and dist.is_initialized():
+        import torch
+        t = torch.tensor([ms, fr], dtype=torch.float64, device=device)
+        m = t.clone()
+        dist.all_reduce(m, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        ms, fr = float(m[0]), float(t[1])
+    return ms, fr / (ms / 1e3)
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if ws == 1:
@@ -211,12 +225,7 @@ def main() -> None:
         torch.cuda.synchronize(dev)
         barrier()
     prof = plan.profile_end()
-    ms_step = e0.elapsed_time(e1) / a.steps
-    if dist is not None:
-        t = torch.tensor([ms_step], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_step = float(t.item())
-    value = F * ws / (ms_step / 1e3)
+    ms_step, value = aggregate(e0.elapsed_time(e1) / a.steps, F, dist, dev)
 
     # per-stage averages inside the timed region
     stages: dict[str, list[float]] = {}
@@ -254,11 +263,7 @@ def main() -> None:
     t0 = time.perf_counter()
     for _ in range(e2e_steps):
         e2e_step()
-    e2e_s = (time.perf_counter() - t0) / e2e_steps
-    if dist is not None:
-        t = torch.tensor([e2e_s], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_ms, e2e_value = aggregate(1e3 * (time.perf_counter() - t0) / e2e_steps, F, dist, dev)
 
     # ---------------------------------------------------------------- roofline of the dominant kernel
     pk = _peaks()
@@ -287,7 +292,7 @@ def main() -> None:
         "stage_ms": stage_ms, "gpu_launches": launches,
         "roofline": roof, "roofline_svd": roof_svd,
         "clocks": clk.summary(),
-        "e2e": {"value": F * ws / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(w.audio.nbytes),
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": int(w.audio.nbytes),
                 "d2h_bytes_per_step": int(2 * F * 8)},
         "setup_seconds": info["setup_seconds"],
     }
