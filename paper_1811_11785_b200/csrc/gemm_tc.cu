@@ -43,6 +43,9 @@ struct GemmParams {
     int ksplit;                            // K splits (mode 1 only; splits fall on chunk boundaries)
     int spc;                               // slabs per chunk
     int prefetch;                          // 0 none, 1 L2 prefetch of the next chunk's phasors, 2 same evict_last
+    int bn;                                // frames per tile of the CTA-pair kernel (multiple of 32, <= 256)
+    int dbg;                               // timing experiments only (SVDPHAT_GEMM_DBG): 1 producer writes zeros,
+                                           // 2 TMA re-loads one W tile (results invalid)
 };
 
 // Work unit t -> output tile (m, n) and the slab / chunk range of its K split.
@@ -366,13 +369,15 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
 // TMA-loads rows [m*256 + 128r, +128) of A and its 4 producer warps build frames [n*256 + 128r, +128) of B; the
 // even (leader) CTA issues tcgen05.mma.cta_group::2 for both.  Per SM this halves the shared-memory operand
 // traffic of the 1-CTA kernel (ncu r01: ~192 B/clk/SM needed at full MMA rate), the reason for the pair.
-// Warps: 0 TMA (+TMEM alloc), 1 MMA (leader), 2-3 idle, 4-7 epilogue (lane groups 0-3), 8-11 producer.
+// Warps: 0 TMA (+TMEM alloc), 1 MMA (leader), 2-5 epilogue (lane groups 2,3,0,1), 6-9 producer.  The producer
+// keeps the frame's phasors of the current bin chunk in registers.  (Register double-buffering of the next chunk
+// was tried and removed: the apparent 'load cost' was power - zeroed operands keep the clock high under the cap.)
 // ================================================================================================================
 constexpr int STAGES2 = 6;
 constexpr int A2_BYTES = 128 * BK * 2;                 // 16 KB: this CTA's half of the 256 A rows
 constexpr int B2_BYTES = 128 * BK * 2;                 // 16 KB: this CTA's half of the 256 frames
 constexpr int NPW2 = 4;                                // producer warps per CTA (128 frames)
-constexpr int THREADS2 = 32 * (8 + NPW2);
+constexpr int THREADS2 = 32 * (6 + NPW2);
 constexpr int SMEM2_BYTES = 1024 + STAGES2 * (A2_BYTES + B2_BYTES) + 256;
 
 template <int Mi, int BPC, int MODE>
@@ -382,7 +387,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     constexpr int kPairs = Mi * (Mi - 1) / 2;
     constexpr int kUnitsRaw = (BPC == 4) ? kPairs : (kPairs + 1) / 2;
     constexpr int kU = (kUnitsRaw + 7) / 8 * 8;
-    constexpr uint32_t kIdesc = umma_idesc_f16(256, 256);
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -400,6 +404,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     const bool leader = rank == 0;
     const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
     const int units = p.m_tiles * p.n_tiles * p.ksplit;   // m_tiles counts 256-row pair tiles
+    const int bn = p.bn, hb = p.bn / 2;                    // frames per pair tile / per CTA
+    const uint32_t idesc = umma_idesc_f16(256, (uint32_t)bn);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < STAGES2; ++s) {
@@ -434,9 +440,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                 for (int ks = w.k0; ks < w.k1; ++ks) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
-                    tma_load_2d_2sm(sA + stage * A2_BYTES, &tmA, ks * BK, w.m * 256 + (int)rank * 128, &full[stage]);
+                    tma_load_2d_2sm(sA + stage * A2_BYTES, &tmA, (p.dbg & 2) ? 0 : ks * BK, (p.dbg & 2) ? (int)rank * 128 : w.m * 256 + (int)rank * 128, &full[stage]);
                     if (!kProducer)
-                        tma_load_2d_2sm(sB + stage * B2_BYTES, &tmB, ks * BK, w.n * BN + (int)rank * 128, &full[stage]);
+                        tma_load_2d_2sm(sB + stage * B2_BYTES, &tmB, ks * BK, w.n * bn + (int)rank * hb, &full[stage]);
                     if (++stage == STAGES2) {
                         stage = 0;
                         phase ^= 1;
@@ -463,7 +469,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                         const uint32_t b0 = smem_u32(sB + stage * B2_BYTES);
 #pragma unroll
                         for (int kk = 0; kk < BK / 16; ++kk)
-                            umma_f16_2sm(d_tmem, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), kIdesc,
+                            umma_f16_2sm(d_tmem, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), idesc,
                                          (ks != w.k0) || (kk != 0));
                         umma_commit_2sm(&empty[stage], 0x3);
                     }
@@ -481,7 +487,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                 }
             }
         }
-    } else if (warp >= 4 && warp < 8) {
+    } else if (warp >= 2 && warp < 6) {
         const int g = warp & 3;
         int acc = 0;
         uint32_t acc_phase = 0;
@@ -493,11 +499,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
             const int row = w.m * 256 + (int)rank * 128 + g * 32 + lane;
             const bool row_ok = row < p.rows_valid;
 #pragma unroll 1
-            for (int j0 = 0; j0 < BN; j0 += 32) {
+            for (int j0 = 0; j0 < bn; j0 += 32) {
                 uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + acc * BN + j0, r);
                 tmem_ld_wait();
-                const int f0 = w.n * BN + j0;
+                const int f0 = w.n * bn + j0;
                 if (MODE == 1) {
                     if (row_ok) {
 #pragma unroll
@@ -523,9 +529,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                 acc_phase ^= 1;
             }
         }
-    } else if (warp >= 8 && kProducer) {
+    } else if (warp >= 6 && kProducer) {
         constexpr PairTab<Mi> PT{};
-        const int tp = (warp - 8) * 32 + lane;                    // frame row of this CTA's half tile: 0..127
+        const int tp = (warp - 6) * 32 + lane;                    // frame row of this CTA's half tile: 0..127
         const uint32_t row_off = (uint32_t)((tp >> 3) * 1024 + (tp & 7) * 128);
         const uint32_t xr = (uint32_t)(tp & 7);
         int stage = 0;
@@ -533,8 +539,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
         constexpr int kUB = BPC * 4;
         for (int t = pair; t < units; t += n_pairs) {
             const Unit w = unit_of(p, t);
-            const int f = w.n * BN + (int)rank * 128 + tp;
-            const bool valid = f < p.F;
+            const int f = w.n * bn + (int)rank * hb + tp;
+            const bool valid = f < p.F && tp < hb && !(p.dbg & 1);
 #pragma unroll 1
             for (int c = w.c0; c < w.c1; ++c) {
                 uint32_t e[Mi][BPC];
@@ -672,6 +678,16 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
     gp.ldz = 2 * p.Dh;
     gp.ksplit = 1;
     gp.spc = p.L.U / 8;
+    gp.bn = BN;
+    static const int dbg = [] {
+        const char* e = getenv("SVDPHAT_GEMM_DBG");
+        return e ? atoi(e) : 0;
+    }();
+    gp.dbg = dbg;
+    static const int fixed_bn = [] {
+        const char* e = getenv("SVDPHAT_PAIR_BN");
+        return e ? atoi(e) : 0;
+    }();
     static const int pf = [] {
         const char* e = getenv("SVDPHAT_GEMM_PREFETCH");
         return e ? atoi(e) : 1;
@@ -707,8 +723,22 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
     if (mode == 2) return launch_one<4, 4, 2>(*A, *B, gp, grid, s);
     if (mode == 0 && p.pair_srp) {
         gp.m_tiles = p.Q_pad / 256;
+        // frames per pair tile: 256 unless SVDPHAT_PAIR_BN picks another multiple of 32 (r01 measurement: the
+        // wave-quantisation optimum 224 ran slower at cfg3 under the power cap than 256)
+        const int npairs = p.num_sms / 2;
+        long best = -1;
+        for (int bn = 256; bn >= 128; bn -= 32) {
+            if (bn != (fixed_bn ? fixed_bn : 256)) continue;
+            const long nt = (F + bn - 1) / bn;
+            const long waves = (gp.m_tiles * nt + npairs - 1) / npairs;
+            if (best < 0 || waves * bn < best) {
+                best = waves * bn;
+                gp.bn = bn;
+                gp.n_tiles = (int)nt;
+            }
+        }
         const int units = gp.m_tiles * gp.n_tiles;
-        const int pairs = units < p.num_sms / 2 ? units : p.num_sms / 2;
+        const int pairs = units < npairs ? units : npairs;
 #define SVD_DISPATCH2(MI, BP)                                                                                \
     if (p.L.Mi == MI) {                                                                                     \
         gemm2_kernel<MI, BP, 0><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(*A, *B, gp);                        \

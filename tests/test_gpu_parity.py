@@ -183,3 +183,59 @@ def test_degenerate_and_duplicates():
         assert np.all(q[:4] == -1) and np.all(q[5:9] == -1), q
         assert np.all((q[9:] >= 0) & (q[9:] < 100)), q
     plan.close()
+
+
+def test_cfg4_srp_full_batch_sampled():
+    """M = 32 (two pairs per 16-byte unit, bpc = 2), random-cube array, two sources per frame."""
+    w = make(4)
+    plan = _plan(w, methods=("srp",))
+    audio = torch.from_numpy(w.audio).to(DEV)
+    q, s = _run(plan, w, "srp", audio, w.n_frames)
+    rng = np.random.default_rng(4)
+    sub = np.sort(np.concatenate([rng.choice(w.n_frames, 14, replace=False), [0, w.n_frames - 1]]))
+    tau = srp.tdoa(w.mics, w.points, w.fs, w.c, w.field)
+    x = srp.frames_to_x(PP._frames_subset(w, sub))
+    P_, Y_at = PP.srp_reference(tau, x, w.N)
+    print(PP.compare(q[sub], s[sub], P_, Y_at, "cfg4 SRP"))
+    plan.close()
+
+
+@pytest.mark.parametrize("M,N,level,field", [(2, 64, 2, "far"), (3, 32, 1, "far"), (5, 16, 2, "far"),
+                                             (6, 128, 2, "near"), (7, 256, 3, "far"), (12, 64, 2, "far"),
+                                             (20, 128, 1, "near"), (32, 64, 1, "far")])
+def test_small_random_arrays(M, N, level, field):
+    """Mic counts that are not instantiated (padded to 4/8/16/32), small N (direct-DFT path for N < 64), near
+    field; all frames against the oracle for both methods."""
+    from workloads import geometry as G
+    from workloads import scenes as SC
+    rng = np.random.default_rng(1000 + M + N)
+    mics = rng.uniform(-0.08, 0.08, (M, 3))
+    pts = G.icosphere(level)
+    if field == "near":
+        pts = pts * 1.5 + np.array([0.0, 0.0, 0.2])
+    hop = N // 2
+    F = 37
+    L = (F - 1) * hop + N
+    src = pts[rng.integers(len(pts))]
+    u = src / np.linalg.norm(src)
+    audio = (SC.plane_wave_stream(rng, mics, 16000.0, 343.0, L, u, 10.0)
+             if field == "far" else SC.point_source_stream(rng, mics, 16000.0, 343.0, L, src, 10.0)).astype(np.float32)
+    plan = S.Plan(mics, pts, 16000.0, 343.0, N, hop, field, delta=1e-5, methods=("srp", "svd"), max_frames=F)
+    tau = srp.tdoa(mics, pts, 16000.0, 343.0, field)
+    fac = svd.svd_factors(tau, N, 1e-5)
+    assert plan.info()["D"] == fac["D"]
+    fr = srp.extract_frames(audio, F, M, N, L, hop)
+    x = srp.frames_to_x(fr)
+    d_audio = torch.from_numpy(audio).to(DEV)
+    doa = torch.empty(2 * F, dtype=torch.int32, device=DEV)
+    sc = torch.empty(2 * F, dtype=torch.float32, device=DEV)
+    plan.localize("both", d_audio, F, L, hop, doa, sc, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    q, s = doa.cpu().numpy(), sc.cpu().numpy()
+    keep = _check_degenerate(q[:F], s[:F], x)
+    P_, Y_at = PP.srp_reference(tau, x[keep], N)
+    PP.compare(q[:F][keep], s[:F][keep], P_, Y_at, f"M={M} N={N} SRP")
+    keep = _check_degenerate(q[F:], s[F:], x)
+    P_, Y_at = PP.svd_reference(fac, tau, x[keep], N)
+    PP.compare(q[F:][keep], s[F:][keep], P_, Y_at, f"M={M} N={N} SVD")
+    plan.close()
