@@ -123,6 +123,11 @@ struct svdphat_plan_s {
     Plan p;
     ~svdphat_plan_s() {
         for (cudaEvent_t e : p.prof_ev) cudaEventDestroy(e);
+        for (int i = 0; i < 2; ++i) {
+            if (p.ev_copied[i]) cudaEventDestroy(p.ev_copied[i]);
+            if (p.ev_done[i]) cudaEventDestroy(p.ev_done[i]);
+        }
+        if (p.copy_stream) cudaStreamDestroy(p.copy_stream);
         void* bufs[] = {p.d_W16, p.d_V16, p.d_R16, p.d_rep, p.d_delay, p.d_window, p.d_twN, p.d_P16,
                         p.d_keys, p.d_Z32, p.d_Zs16, p.d_zflag, p.d_stage, p.d_doa_stage, p.d_score_stage};
         for (void* b : bufs)
@@ -312,8 +317,8 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     const int64_t bytes_P16 = (int64_t)p.L.n_chunks * p.L.Mi * Fp * p.L.unit_bytes;
     SVD_CUDA_TRY(cudaMalloc(&p.d_P16, bytes_P16));
     SVD_CUDA_TRY(cudaMemset(p.d_P16, 0, bytes_P16));
-    SVD_CUDA_TRY(cudaMalloc(&p.d_keys, Fp * sizeof(unsigned long long)));
-    p.bytes_ws = bytes_P16 + Fp * 8;
+    SVD_CUDA_TRY(cudaMalloc(&p.d_keys, 2 * Fp * sizeof(unsigned long long)));
+    p.bytes_ws = bytes_P16 + 2 * Fp * 8;
     if (p.methods & SVDPHAT_METHOD_SVD) {
         SVD_CUDA_TRY(cudaMalloc(&p.d_Z32, MAX_KSPLIT * Fp * 2 * p.Dh * sizeof(float)));
         SVD_CUDA_TRY(cudaMemset(p.d_Z32, 0, MAX_KSPLIT * Fp * 2 * p.Dh * sizeof(float)));
@@ -366,45 +371,53 @@ svdphat_status svdphat_plan_sigma2(svdphat_plan_t plan, double* out, int32_t n) 
     return SVDPHAT_OK;
 }
 
+static svdphat_status localize_impl(Plan& p, int32_t method, const float* d_audio, int F, int64_t channel_stride,
+                                    int64_t frame_stride, int32_t* doa_srp, float* sc_srp, int32_t* doa_svd,
+                                    float* sc_svd, cudaStream_t s) {
+    SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_STFT, s,
+                        [&] { return launch_stft_phat(p, d_audio, channel_stride, frame_stride, F, s); }));
+    if (method & SVDPHAT_METHOD_SRP) {
+        SVD_CUDA_TRY(cudaMemsetAsync(p.d_keys, 0, (size_t)F * 8, s));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_GEMM, s, [&] { return launch_gemm(p, 0, F, s); }));
+    }
+    if (method & SVDPHAT_METHOD_SVD) {
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_PROJ, s, [&] { return launch_gemm(p, 1, F, s); }));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_NORM, s, [&] { return launch_zsplit(p, F, s); }));
+        SVD_CUDA_TRY(cudaMemsetAsync(p.d_keys + p.F_pad, 0, (size_t)F * 8, s));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_SEARCH, s, [&] { return launch_gemm(p, 2, F, s); }));
+    }
+    int32_t* const doas[2] = {doa_srp, doa_svd};
+    float* const scores[2] = {sc_srp, sc_svd};
+    SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_FINALIZE, s, [&] { return launch_finalize(p, method, F, doas, scores, s); }));
+    p.last_frames = F;
+    p.last_method = method;
+    return SVDPHAT_OK;
+}
+
+static svdphat_status check_localize_args(Plan& p, int32_t method, int64_t n_frames, int64_t cs, int64_t fs) {
+    if (method < SVDPHAT_METHOD_SRP || method > SVDPHAT_METHOD_BOTH)
+        return fail(SVDPHAT_INVALID_ARG, "method must be SRP, SVD or BOTH");
+    if ((p.methods & method) != method) return fail(SVDPHAT_INVALID_ARG, "method was not planned");
+    if (n_frames < 0 || n_frames > p.max_frames) return fail(SVDPHAT_INVALID_ARG, "n_frames out of [0, max_frames]");
+    if (cs < 0 || fs < 0) return fail(SVDPHAT_INVALID_ARG, "negative stride");
+    return SVDPHAT_OK;
+}
+
 svdphat_status svdphat_localize(svdphat_plan_t plan, int32_t method, const float* d_audio, int64_t n_frames,
                                 int64_t channel_stride, int64_t frame_stride, int32_t* d_doa, float* d_score,
                                 void* stream) {
     if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
     Plan& p = plan->p;
-    if (method < SVDPHAT_METHOD_SRP || method > SVDPHAT_METHOD_BOTH)
-        return fail(SVDPHAT_INVALID_ARG, "method must be SRP, SVD or BOTH");
-    if ((p.methods & method) != method) return fail(SVDPHAT_INVALID_ARG, "method was not planned");
-    if (n_frames < 0 || n_frames > p.max_frames) return fail(SVDPHAT_INVALID_ARG, "n_frames out of [0, max_frames]");
+    svdphat_status st = check_localize_args(p, method, n_frames, channel_stride, frame_stride);
+    if (st != SVDPHAT_OK) return st;
     if (n_frames == 0) return SVDPHAT_OK;
     if (!d_audio || !d_doa || !d_score) return fail(SVDPHAT_INVALID_ARG, "NULL buffer");
-    if (channel_stride < 0 || frame_stride < 0) return fail(SVDPHAT_INVALID_ARG, "negative stride");
     if (reinterpret_cast<uintptr_t>(d_audio) & 3) return fail(SVDPHAT_INVALID_ARG, "d_audio not 4-byte aligned");
-    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    const int F = (int)n_frames;
     SVD_CUDA_TRY(cudaSetDevice(p.device));
-    SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_STFT, s,
-                        [&] { return launch_stft_phat(p, d_audio, channel_stride, frame_stride, F, s); }));
-    int32_t* doa = d_doa;
-    float* score = d_score;
-    if (method & SVDPHAT_METHOD_SRP) {
-        SVD_CUDA_TRY(cudaMemsetAsync(p.d_keys, 0, (size_t)F * 8, s));
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_GEMM, s, [&] { return launch_gemm(p, 0, F, s); }));
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_FINALIZE, s,
-                            [&] { return launch_finalize(p, SVDPHAT_METHOD_SRP, F, doa, score, s); }));
-        doa += F;
-        score += F;
-    }
-    if (method & SVDPHAT_METHOD_SVD) {
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_PROJ, s, [&] { return launch_gemm(p, 1, F, s); }));
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_NORM, s, [&] { return launch_zsplit(p, F, s); }));
-        SVD_CUDA_TRY(cudaMemsetAsync(p.d_keys, 0, (size_t)F * 8, s));
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_SEARCH, s, [&] { return launch_gemm(p, 2, F, s); }));
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_FINALIZE, s,
-                            [&] { return launch_finalize(p, SVDPHAT_METHOD_SVD, F, doa, score, s); }));
-    }
-    p.last_frames = F;
-    p.last_method = method;
-    return SVDPHAT_OK;
+    const int F = (int)n_frames;
+    const bool both = method == SVDPHAT_METHOD_BOTH;
+    return localize_impl(p, method, d_audio, F, channel_stride, frame_stride, d_doa, d_score,
+                         both ? d_doa + F : d_doa, both ? d_score + F : d_score, reinterpret_cast<cudaStream_t>(stream));
 }
 
 svdphat_status svdphat_profile_begin(svdphat_plan_t plan, int32_t capacity) {
@@ -446,34 +459,67 @@ svdphat_status svdphat_localize_host(svdphat_plan_t plan, int32_t method, const 
                                      float* h_score, void* stream) {
     if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
     Plan& p = plan->p;
-    if (n_frames < 0 || n_frames > p.max_frames) return fail(SVDPHAT_INVALID_ARG, "n_frames out of [0, max_frames]");
+    svdphat_status st = check_localize_args(p, method, n_frames, channel_stride, frame_stride);
+    if (st != SVDPHAT_OK) return st;
     if (n_frames == 0) return SVDPHAT_OK;
     if (!h_audio || !h_doa || !h_score || audio_elems <= 0) return fail(SVDPHAT_INVALID_ARG, "NULL/empty buffer");
-    const int64_t need = (int64_t)(p.M - 1) * channel_stride + (n_frames - 1) * frame_stride + p.N;
+    const int64_t M1 = p.M - 1;
+    const int64_t need = M1 * channel_stride + (n_frames - 1) * frame_stride + p.N;
     if (need > audio_elems) return fail(SVDPHAT_INVALID_ARG, "audio buffer smaller than the addressed frames");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     SVD_CUDA_TRY(cudaSetDevice(p.device));
-    if (audio_elems > p.stage_elems) {
+    const int F = (int)n_frames;
+    // Frame-major buffers (each frame's samples inside its own frame_stride span) are pipelined in chunks of
+    // whole 256-frame tiles: the H2D of chunk i+1 (copy stream) overlaps the kernels of chunk i (caller stream).
+    const int64_t span1 = M1 * channel_stride + p.N;            // elements touched by one frame
+    const bool frame_major = frame_stride >= span1;
+    int chunk = F;
+    if (frame_major && F >= 2048) chunk = (int)std::min<int64_t>(F, ((F + 3) / 4 + 255) / 256 * 256);
+    const int nchunks = (F + chunk - 1) / chunk;
+    const int64_t slot_elems = nchunks == 1 ? need : (int64_t)(chunk - 1) * frame_stride + span1;
+    if (slot_elems > p.stage_elems) {
         if (p.d_stage) cudaFree(p.d_stage);
         p.d_stage = nullptr;
         p.stage_elems = 0;
-        if (cudaMalloc(&p.d_stage, audio_elems * sizeof(float)) != cudaSuccess)
+        if (cudaMalloc(&p.d_stage, 2 * slot_elems * sizeof(float)) != cudaSuccess)
             return fail(SVDPHAT_ALLOC, "staging buffer allocation failed");
-        p.stage_elems = audio_elems;
+        p.stage_elems = slot_elems;
     }
     if (!p.d_doa_stage) {
         if (cudaMalloc(&p.d_doa_stage, 2 * p.F_pad * sizeof(int32_t)) != cudaSuccess ||
             cudaMalloc(&p.d_score_stage, 2 * p.F_pad * sizeof(float)) != cudaSuccess)
             return fail(SVDPHAT_ALLOC, "result staging allocation failed");
     }
-    SVD_CUDA_TRY(cudaMemcpyAsync(p.d_stage, h_audio, audio_elems * sizeof(float), cudaMemcpyHostToDevice, s));
-    svdphat_status st = svdphat_localize(plan, method, p.d_stage, n_frames, channel_stride, frame_stride,
-                                         p.d_doa_stage, p.d_score_stage, stream);
-    if (st != SVDPHAT_OK) return st;
-    const int64_t nout = (method == SVDPHAT_METHOD_BOTH ? 2 : 1) * n_frames;
+    if (!p.copy_stream) {
+        SVD_CUDA_TRY(cudaStreamCreateWithFlags(&p.copy_stream, cudaStreamNonBlocking));
+        for (int i = 0; i < 2; ++i) {
+            SVD_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_copied[i], cudaEventDisableTiming));
+            SVD_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_done[i], cudaEventDisableTiming));
+        }
+    }
+    const bool both = method == SVDPHAT_METHOD_BOTH;
+    SVD_CUDA_TRY(cudaEventRecord(p.ev_done[0], s));            // copy stream starts after prior work on s
+    SVD_CUDA_TRY(cudaEventRecord(p.ev_done[1], s));
+    for (int i = 0; i < nchunks; ++i) {
+        const int slot = i & 1;
+        const int f0 = i * chunk, n = std::min(chunk, F - f0);
+        const int64_t off = (int64_t)f0 * frame_stride;
+        const int64_t elems = nchunks == 1 ? need : (int64_t)(n - 1) * frame_stride + span1;
+        float* dst = p.d_stage + slot * p.stage_elems;
+        SVD_CUDA_TRY(cudaStreamWaitEvent(p.copy_stream, p.ev_done[slot], 0));
+        SVD_CUDA_TRY(cudaMemcpyAsync(dst, h_audio + off, elems * sizeof(float), cudaMemcpyHostToDevice, p.copy_stream));
+        SVD_CUDA_TRY(cudaEventRecord(p.ev_copied[slot], p.copy_stream));
+        SVD_CUDA_TRY(cudaStreamWaitEvent(s, p.ev_copied[slot], 0));
+        st = localize_impl(p, method, dst, n, channel_stride, frame_stride, p.d_doa_stage + f0, p.d_score_stage + f0,
+                           p.d_doa_stage + (both ? F : 0) + f0, p.d_score_stage + (both ? F : 0) + f0, s);
+        if (st != SVDPHAT_OK) return st;
+        SVD_CUDA_TRY(cudaEventRecord(p.ev_done[slot], s));
+    }
+    const int64_t nout = (both ? 2 : 1) * (int64_t)F;
     SVD_CUDA_TRY(cudaMemcpyAsync(h_doa, p.d_doa_stage, nout * sizeof(int32_t), cudaMemcpyDeviceToHost, s));
     SVD_CUDA_TRY(cudaMemcpyAsync(h_score, p.d_score_stage, nout * sizeof(float), cudaMemcpyDeviceToHost, s));
     SVD_CUDA_TRY(cudaStreamSynchronize(s));
+    p.last_frames = F;
     return SVDPHAT_OK;
 }
 
@@ -491,7 +537,8 @@ svdphat_status svdphat_debug_dump(svdphat_plan_t plan, int32_t what, int64_t n_f
     }
     if (what == SVDPHAT_DUMP_KEYS) {
         if (bytes < (int64_t)F * 8) return fail(SVDPHAT_INVALID_ARG, "buffer too small");
-        SVD_CUDA_TRY(cudaMemcpy(host_out, p.d_keys, (size_t)F * 8, cudaMemcpyDeviceToHost));
+        SVD_CUDA_TRY(cudaMemcpy(host_out, p.d_keys + (p.last_method == SVDPHAT_METHOD_SVD ? p.F_pad : 0),
+                                (size_t)F * 8, cudaMemcpyDeviceToHost));
         return SVDPHAT_OK;
     }
     if (what == SVDPHAT_DUMP_Z) {

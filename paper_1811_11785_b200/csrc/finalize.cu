@@ -48,31 +48,49 @@ __global__ void zsplit_kernel(float* __restrict__ Z, int F, int64_t F_pad, int l
 // CTA = 32 consecutive frames (lane = frame, so every phasor record load is a coalesced 512-byte row) x 8 warps
 // striding over the bin chunks; partial sums meet in shared memory.
 constexpr int FIN_WARPS = 8;
+// One or two methods per launch: method slot j in [0, nm) reads keys[j] and writes doa[j]/score[j]; the phasor
+// records of the frame are read once for both.
+struct FinOut {
+    const unsigned long long* keys[2];
+    const int* zflag[2];
+    int32_t* doa[2];
+    float* score[2];
+};
+
+template <int NM>
 __global__ void __launch_bounds__(32 * FIN_WARPS)
-    finalize_kernel(const unsigned long long* __restrict__ keys, const uint8_t* __restrict__ P16, int F,
-                    int64_t F_pad, int M, int Mi, int bpc, int n_chunks, int Kb, int N,
-                    const int* __restrict__ rep, const float* __restrict__ delay, const int* __restrict__ zflag,
-                    int32_t* __restrict__ doa, float* __restrict__ score) {
-    __shared__ float s_y[FIN_WARPS][32];
+    finalize_kernel(FinOut o, const uint8_t* __restrict__ P16, int F, int64_t F_pad, int M, int Mi, int bpc,
+                    int n_chunks, int Kb, int N, const int* __restrict__ rep, const float* __restrict__ delay) {
+    __shared__ float s_y[NM][FIN_WARPS][32];
     __shared__ int s_p[FIN_WARPS][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int f = blockIdx.x * 32 + lane;
     const bool valid = f < F;
-    const unsigned long long key = valid ? keys[f] : 0ull;
-    const int cls = key ? (int)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull)) : -1;
-    const int q = cls >= 0 ? rep[cls] : -1;
-    const float* dq = delay + (int64_t)(q >= 0 ? q : 0) * M;
+    int q[NM];
+    const float* dq[NM];
+#pragma unroll
+    for (int j = 0; j < NM; ++j) {
+        const unsigned long long key = valid ? o.keys[j][f] : 0ull;
+        const int cls = key ? (int)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull)) : -1;
+        q[j] = cls >= 0 ? rep[cls] : -1;
+        dq[j] = delay + (int64_t)(q[j] >= 0 ? q[j] : 0) * M;
+    }
     const int ub = bpc * 4;
     const float inv2N = 2.0f / (float)N;
-    float ysum = 0.f;
+    float ysum[NM];
+#pragma unroll
+    for (int j = 0; j < NM; ++j) ysum[j] = 0.f;
     int pairs = 0;
     if (valid) {
         for (int cc = warp; cc < n_chunks; cc += FIN_WARPS) {
-            float ar[4] = {0, 0, 0, 0}, ai[4] = {0, 0, 0, 0};
+            float ar[NM][4], ai[NM][4];
             int nk[4] = {0, 0, 0, 0};
+#pragma unroll
+            for (int j = 0; j < NM; ++j)
+#pragma unroll
+                for (int t = 0; t < 4; ++t) ar[j][t] = ai[j][t] = 0.f;
             const int kb0 = cc * bpc;
             for (int m = 0; m < M; ++m) {
-                const float dl = __ldg(dq + m);
                 const uint8_t* rec = P16 + (((int64_t)cc * Mi + m) * F_pad + f) * ub;
                 float er[4], ei[4];
                 if (bpc == 4) {
@@ -90,45 +108,55 @@ __global__ void __launch_bounds__(32 * FIN_WARPS)
                     er[0] = r01.x; er[1] = r01.y; ei[0] = i01.x; ei[1] = i01.y;
                     er[2] = er[3] = ei[2] = ei[3] = 0.f;
                 }
-                // e^{+j 2 pi k delta_m / N} for k = kb0 .. kb0+bpc-1: base rotation, then unit steps
-                float bs, bc, ss, sc;
-                sincospif((float)kb0 * dl * inv2N, &bs, &bc);
-                sincospif(dl * inv2N, &ss, &sc);
 #pragma unroll
-                for (int t = 0; t < 4; ++t) {
-                    if (t < bpc && (er[t] != 0.f || ei[t] != 0.f)) {
-                        ar[t] += er[t] * bc - ei[t] * bs;
-                        ai[t] += er[t] * bs + ei[t] * bc;
-                        nk[t] += 1;
+                for (int t = 0; t < 4; ++t)
+                    if (t < bpc && (er[t] != 0.f || ei[t] != 0.f)) nk[t] += 1;
+#pragma unroll
+                for (int j = 0; j < NM; ++j) {
+                    // e^{+j 2 pi k delta_m / N} for k = kb0 .. kb0+bpc-1: base rotation, then unit steps
+                    const float dl = __ldg(dq[j] + m);
+                    float bs, bc, ss, sc;
+                    sincospif((float)kb0 * dl * inv2N, &bs, &bc);
+                    sincospif(dl * inv2N, &ss, &sc);
+#pragma unroll
+                    for (int t = 0; t < 4; ++t) {
+                        if (t < bpc) {
+                            ar[j][t] += er[t] * bc - ei[t] * bs;
+                            ai[j][t] += er[t] * bs + ei[t] * bc;
+                        }
+                        const float nb = bc * sc - bs * ss;
+                        bs = bs * sc + bc * ss;
+                        bc = nb;
                     }
-                    const float nb = bc * sc - bs * ss;
-                    bs = bs * sc + bc * ss;
-                    bc = nb;
                 }
             }
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
                 if (t < bpc && kb0 + t < Kb) {
-                    ysum += ar[t] * ar[t] + ai[t] * ai[t] - (float)nk[t];
+#pragma unroll
+                    for (int j = 0; j < NM; ++j) ysum[j] += ar[j][t] * ar[j][t] + ai[j][t] * ai[j][t] - (float)nk[t];
                     pairs += nk[t] * (nk[t] - 1) / 2;
                 }
             }
         }
     }
-    s_y[warp][lane] = ysum;
+#pragma unroll
+    for (int j = 0; j < NM; ++j) s_y[j][warp][lane] = ysum[j];
     s_p[warp][lane] = pairs;
     __syncthreads();
     if (warp == 0 && valid) {
-        float y = 0.f;
         int pr = 0;
 #pragma unroll
-        for (int w = 0; w < FIN_WARPS; ++w) {
-            y += s_y[w][lane];
-            pr += s_p[w][lane];
+        for (int w = 0; w < FIN_WARPS; ++w) pr += s_p[w][lane];
+#pragma unroll
+        for (int j = 0; j < NM; ++j) {
+            float y = 0.f;
+#pragma unroll
+            for (int w = 0; w < FIN_WARPS; ++w) y += s_y[j][w][lane];
+            const bool dead = (pr == 0) || q[j] < 0 || (o.zflag[j] != nullptr && o.zflag[j][f] != 0);
+            o.doa[j][f] = dead ? -1 : q[j];
+            o.score[j][f] = dead ? 0.f : 0.5f * y;
         }
-        const bool dead = (pr == 0) || q < 0 || (zflag != nullptr && zflag[f] != 0);
-        doa[f] = dead ? -1 : q;
-        score[f] = dead ? 0.f : 0.5f * y;
     }
 }
 
@@ -142,11 +170,32 @@ cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_finalize(const Plan& p, int method, int F, int32_t* doa, float* score, cudaStream_t s) {
+cudaError_t launch_finalize(const Plan& p, int method, int F, int32_t* const doa[2], float* const score[2],
+                            cudaStream_t s) {
     if (F <= 0) return cudaSuccess;
-    finalize_kernel<<<(F + 31) / 32, 32 * FIN_WARPS, 0, s>>>(p.d_keys, p.d_P16, F, p.F_pad, p.M, p.L.Mi, p.L.bpc, p.L.n_chunks,
-                                               p.Kb, p.N, p.d_rep, p.d_delay,
-                                               method == SVDPHAT_METHOD_SVD ? p.d_zflag : nullptr, doa, score);
+    FinOut o{};
+    int nm = 0;
+    if (method & SVDPHAT_METHOD_SRP) {
+        o.keys[nm] = p.d_keys;
+        o.zflag[nm] = nullptr;
+        o.doa[nm] = doa[0];
+        o.score[nm] = score[0];
+        ++nm;
+    }
+    if (method & SVDPHAT_METHOD_SVD) {
+        o.keys[nm] = p.d_keys + p.F_pad;
+        o.zflag[nm] = p.d_zflag;
+        o.doa[nm] = doa[1];
+        o.score[nm] = score[1];
+        ++nm;
+    }
+    const dim3 grid((F + 31) / 32), block(32 * FIN_WARPS);
+    if (nm == 2)
+        finalize_kernel<2><<<grid, block, 0, s>>>(o, p.d_P16, F, p.F_pad, p.M, p.L.Mi, p.L.bpc, p.L.n_chunks, p.Kb,
+                                                  p.N, p.d_rep, p.d_delay);
+    else
+        finalize_kernel<1><<<grid, block, 0, s>>>(o, p.d_P16, F, p.F_pad, p.M, p.L.Mi, p.L.bpc, p.L.n_chunks, p.Kb,
+                                                  p.N, p.d_rep, p.d_delay);
     return cudaGetLastError();
 }
 

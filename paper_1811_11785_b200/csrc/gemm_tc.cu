@@ -615,6 +615,240 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     }
 }
 
+// ================================================================================================================
+// CTA-pair SRP GEMM with the cross-spectrum in TMEM ("TS" MMA).  Frames on M: CTA r's 4 producer warps write the
+// frames [n*256 + 128r, +128) of X straight into TMEM (lane = frame) with tcgen05.st, one 64-element K slab per
+// store, so X never touches shared memory; W is the B operand (N = 256 rows per pair, 128 per CTA) streamed by 2-SM
+// TMA.  The accumulator (128 frames x 256 rows per CTA) is reduced by a per-thread running argmax over its columns.
+// TMEM (512 cols): [0,256) accumulator, [256,512) 8-slot X ring of 32 columns.  Smem: 10-slot W ring.
+// Warps: 0 TMA (+TMEM alloc), 1 MMA (leader), 2-5 epilogue (lane groups 2,3,0,1), 6-9 producer (same groups).
+// ================================================================================================================
+constexpr int W3_STAGES = 10;
+constexpr int X3_STAGES = 8;
+constexpr int W3_BYTES = 128 * BK * 2;                 // 16 KB: this CTA's 128 rows of W per slab
+constexpr int THREADS3 = 32 * 10;
+constexpr int SMEM3_BYTES = 1024 + W3_STAGES * W3_BYTES + 512;
+
+template <int Mi, int BPC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS3, 1)
+    gemm3_kernel(const __grid_constant__ CUtensorMap tmW, GemmParams p) {
+    constexpr int kPairs = Mi * (Mi - 1) / 2;
+    constexpr int kUnitsRaw = (BPC == 4) ? kPairs : (kPairs + 1) / 2;
+    constexpr int kU = (kUnitsRaw + 7) / 8 * 8;
+    constexpr uint32_t kIdesc = umma_idesc_f16(256, 256);
+
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sW = smem;
+    uint64_t* wfull = reinterpret_cast<uint64_t*>(sW + W3_STAGES * W3_BYTES);
+    uint64_t* wempty = wfull + W3_STAGES;
+    uint64_t* xfull = wempty + W3_STAGES;
+    uint64_t* xempty = xfull + X3_STAGES;
+    uint64_t* tfull = xempty + X3_STAGES;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+    const int units = p.m_tiles * p.n_tiles;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < W3_STAGES; ++s) {
+            mbar_init(&wfull[s], 1);
+            mbar_init(&wempty[s], 1);
+        }
+        for (int s = 0; s < X3_STAGES; ++s) {
+            mbar_init(&xfull[s], 8);        // 4 producer warps x 2 CTAs (only the leader's is used)
+            mbar_init(&xempty[s], 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 8);               // 4 epilogue warps x 2 CTAs
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc_2sm<512>(tmem_slot);
+    if (warp == 1 && lane == 0) tma_prefetch_desc(&tmW);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const uint32_t tmem_x = tmem_base + 256;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            for (int t = pair; t < units; t += n_pairs) {
+                const int m = t / p.n_tiles;
+                for (int ks = 0; ks < p.n_slabs; ++ks) {
+                    mbar_wait(&wempty[stage], phase ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&wfull[stage], 2 * W3_BYTES);
+                    tma_load_2d_2sm(sW + stage * W3_BYTES, &tmW, ks * BK, m * 256 + (int)rank * 128, &wfull[stage]);
+                    if (++stage == W3_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader) {
+            int ws = 0, xs = 0;
+            uint32_t wph = 0, xph = 0, tph = 0;
+            for (int t = pair; t < units; t += n_pairs) {
+                mbar_wait(tempty, tph ^ 1);
+                tph ^= 1;
+                tc_fence_after();
+                for (int ks = 0; ks < p.n_slabs; ++ks) {
+                    mbar_wait(&wfull[ws], wph);
+                    mbar_wait(&xfull[xs], xph);
+                    tc_fence_after();
+                    if (lane == 0) {
+                        const uint32_t b0 = smem_u32(sW + ws * W3_BYTES);
+                        const uint32_t a0 = tmem_x + xs * 32;
+#pragma unroll
+                        for (int kk = 0; kk < BK / 16; ++kk)
+                            umma_f16_2sm_ts(tmem_base, a0 + kk * 8, umma_desc_sw128(b0 + kk * 32), kIdesc,
+                                            (ks | kk) != 0);
+                        umma_commit_2sm(&wempty[ws], 0x3);
+                        umma_commit_2sm(&xempty[xs], 0x3);
+                    }
+                    __syncwarp();
+                    if (++ws == W3_STAGES) {
+                        ws = 0;
+                        wph ^= 1;
+                    }
+                    if (++xs == X3_STAGES) {
+                        xs = 0;
+                        xph ^= 1;
+                    }
+                }
+                if (lane == 0) umma_commit_2sm(tfull, 0x3);
+                __syncwarp();
+            }
+        }
+    } else if (warp < 6) {
+        // ---- epilogue: lane = frame; running argmax over the 256 W rows of the tile (lowest index on ties)
+        const int g = warp & 3;
+        uint32_t tph = 0;
+        for (int t = pair; t < units; t += n_pairs) {
+            const int m = t / p.n_tiles, n = t % p.n_tiles;
+            mbar_wait(tfull, tph);
+            tph ^= 1;
+            tc_fence_after();
+            const int f = n * 256 + (int)rank * 128 + g * 32 + lane;
+            float best = -INFINITY;
+            int bi = -1;
+            const int rows_left = p.rows_valid - m * 256;
+#pragma unroll 1
+            for (int j0 = 0; j0 < 256; j0 += 32) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + j0, r);
+                tmem_ld_wait();
+#pragma unroll
+                for (int jj = 0; jj < 32; ++jj) {
+                    const float v = __uint_as_float(r[jj]);
+                    if (j0 + jj < rows_left && v > best) {
+                        best = v;
+                        bi = j0 + jj;
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty, 0);
+            if (f < p.F && bi >= 0) atomicMax(&p.keys[f], make_key(best, (uint32_t)(m * 256 + bi)));
+        }
+    } else {
+        // ---- producer: X slabs (eqs. 3, 7) from the frame's phasors into this CTA's TMEM lanes
+        constexpr PairTab<Mi> PT{};
+        const int g = warp & 3;
+        const int row = g * 32 + lane;                                 // TMEM lane = frame row in this CTA
+        constexpr int kUB = BPC * 4;
+        int xs = 0;
+        uint32_t xph = 0;
+        for (int t = pair; t < units; t += n_pairs) {
+            const int n = t % p.n_tiles;
+            const int f = n * 256 + (int)rank * 128 + row;
+            const bool valid = f < p.F;
+#pragma unroll 1
+            for (int c = 0; c < p.n_chunks; ++c) {
+                uint32_t e[Mi][BPC];
+                const uint8_t* src = p.P16 + ((int64_t)c * Mi * p.F_pad + f) * kUB;
+#pragma unroll
+                for (int mm = 0; mm < Mi; ++mm) {
+                    if constexpr (BPC == 4) {
+                        uint4 v = valid ? __ldg(reinterpret_cast<const uint4*>(src + (int64_t)mm * p.F_pad * kUB))
+                                        : make_uint4(0, 0, 0, 0);
+                        e[mm][0] = v.x;
+                        e[mm][1] = v.y;
+                        e[mm][2] = v.z;
+                        e[mm][3] = v.w;
+                    } else {
+                        uint2 v = valid ? __ldg(reinterpret_cast<const uint2*>(src + (int64_t)mm * p.F_pad * kUB))
+                                        : make_uint2(0, 0);
+                        e[mm][0] = v.x;
+                        e[mm][1] = v.y;
+                    }
+                }
+                uint32_t slab[32];
+#pragma unroll
+                for (int u = 0; u < kU; ++u) {
+                    uint32_t* o = &slab[(u & 7) * 4];
+                    if constexpr (BPC == 4) {
+                        if (u < kPairs) {
+                            const int a = PT.i[u], b = PT.j[u];
+                            const uint32_t nra01 = e[a][0] ^ 0x80008000u, nra23 = e[a][1] ^ 0x80008000u;
+                            o[0] = h2fma(e[a][0], e[b][0], h2mul(e[a][2], e[b][2]));
+                            o[1] = h2fma(e[a][1], e[b][1], h2mul(e[a][3], e[b][3]));
+                            o[2] = h2fma(e[a][2], e[b][0], h2mul(nra01, e[b][2]));
+                            o[3] = h2fma(e[a][3], e[b][1], h2mul(nra23, e[b][3]));
+                        } else {
+                            o[0] = o[1] = o[2] = o[3] = 0u;
+                        }
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int pp = 2 * u + h;
+                            if (pp < kPairs) {
+                                const int a = PT.i[pp], b = PT.j[pp];
+                                const uint32_t nra = e[a][0] ^ 0x80008000u;
+                                o[2 * h + 0] = h2fma(e[a][0], e[b][0], h2mul(e[a][1], e[b][1]));
+                                o[2 * h + 1] = h2fma(e[a][1], e[b][0], h2mul(nra, e[b][1]));
+                            } else {
+                                o[2 * h + 0] = o[2 * h + 1] = 0u;
+                            }
+                        }
+                    }
+                    if ((u & 7) == 7) {
+                        mbar_wait(&xempty[xs], xph ^ 1);
+                        tmem_st_32x32b_x32(tmem_x + (uint32_t(g * 32) << 16) + xs * 32, slab);
+                        tmem_st_wait();
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive_cluster(&xfull[xs], 0);
+                        if (++xs == X3_STAGES) {
+                            xs = 0;
+                            xph ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc_2sm<512>(tmem_base);
+    }
+}
+
 // ---------------------------------------------------------------- host side
 template <int Mi, int BPC, int MODE>
 static cudaError_t set_attr_one() {
@@ -634,6 +868,12 @@ cudaError_t gemm_set_attributes() {
     if ((e = set_attr_two<8, 4, 0>()) != cudaSuccess) return e;
     if ((e = set_attr_two<16, 4, 0>()) != cudaSuccess) return e;
     if ((e = set_attr_two<32, 2, 0>()) != cudaSuccess) return e;
+    if ((e = cudaFuncSetAttribute(gemm3_kernel<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_BYTES))) return e;
+    if ((e = cudaFuncSetAttribute(gemm3_kernel<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_BYTES))) return e;
+    if ((e = cudaFuncSetAttribute(gemm3_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_BYTES)))
+        return e;
+    if ((e = cudaFuncSetAttribute(gemm3_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_BYTES)))
+        return e;
 #define SVD_ATTR(MI, B)                                        \
     if ((e = set_attr_one<MI, B, 0>()) != cudaSuccess) return e; \
     if ((e = set_attr_one<MI, B, 1>()) != cudaSuccess) return e;
@@ -708,6 +948,7 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
     } else {
         A = &p.tm_R;
         B = &p.tm_Zs;
+        gp.keys = p.d_keys + p.F_pad;
         gp.n_slabs = p.K2 / BK;
         gp.m_tiles = p.Q_pad / BM;
         gp.rows_valid = p.Q_eff;
@@ -721,6 +962,27 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
     const int grid = tiles < p.num_sms ? tiles : p.num_sms;
     if (tiles == 0) return cudaSuccess;
     if (mode == 2) return launch_one<4, 4, 2>(*A, *B, gp, grid, s);
+    static const int ts = [] {
+        const char* e = getenv("SVDPHAT_SRP_TS");
+        return e ? atoi(e) : 1;
+    }();
+    if (mode == 0 && p.pair_srp && ts) {
+        gp.m_tiles = p.Q_pad / 256;
+        gp.n_tiles = (F + 255) / 256;
+        const int units = gp.m_tiles * gp.n_tiles;
+        const int pairs = units < p.num_sms / 2 ? units : p.num_sms / 2;
+#define SVD_DISPATCH3(MI, BP)                                                          \
+    if (p.L.Mi == MI) {                                                               \
+        gemm3_kernel<MI, BP><<<2 * pairs, THREADS3, SMEM3_BYTES, s>>>(*A, gp);        \
+        return cudaGetLastError();                                                    \
+    }
+        SVD_DISPATCH3(4, 4)
+        SVD_DISPATCH3(8, 4)
+        SVD_DISPATCH3(16, 4)
+        SVD_DISPATCH3(32, 2)
+#undef SVD_DISPATCH3
+        return cudaErrorInvalidValue;
+    }
     if (mode == 0 && p.pair_srp) {
         gp.m_tiles = p.Q_pad / 256;
         // frames per pair tile: 256 unless SVDPHAT_PAIR_BN picks another multiple of 32 (r01 measurement: the

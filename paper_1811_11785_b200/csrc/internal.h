@@ -55,7 +55,7 @@ struct Plan {
     float2* d_twN = nullptr;      // [N]     e^{-j 2 pi k / N}
     // workspace
     uint8_t* d_P16 = nullptr;     // phasors
-    unsigned long long* d_keys = nullptr;  // [F_pad]
+    unsigned long long* d_keys = nullptr;  // [2][F_pad]: SRP keys, SVD search keys
     float* d_Z32 = nullptr;       // [MAX_KSPLIT][F_pad][2*Dh] partial Z of the split-K projection
     __half* d_Zs16 = nullptr;     // [F_pad][K2]
     int* d_zflag = nullptr;       // [F_pad]
@@ -67,9 +67,12 @@ struct Plan {
     alignas(64) CUtensorMap tm_Zs;
     int num_sms = 148;
     bool pair_srp = true;          // SRP GEMM on CTA pairs (cta_group::2); Q_pad is then a multiple of 256
-    // host-buffer path
+    // host-buffer path: two staging slots + a copy stream so chunk i+1's H2D overlaps chunk i's compute
     float* d_stage = nullptr;
-    int64_t stage_elems = 0;
+    int64_t stage_elems = 0;           // elements per slot
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev_copied[2] = {nullptr, nullptr};
+    cudaEvent_t ev_done[2] = {nullptr, nullptr};
     int32_t* d_doa_stage = nullptr;
     float* d_score_stage = nullptr;
     int64_t last_frames = 0;
@@ -102,7 +105,9 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s);
 cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s);
 constexpr int MAX_KSPLIT = 4;
 int ksplit_for(const Plan& p, int tiles);   // K splits of the SVD projection GEMM for its tile count
-cudaError_t launch_finalize(const Plan& p, int method, int F, int32_t* doa, float* score, cudaStream_t s);
+// method SRP|SVD|BOTH; doa[0]/score[0] receive SRP results, doa[1]/score[1] SVD results
+cudaError_t launch_finalize(const Plan& p, int method, int F, int32_t* const doa[2], float* const score[2],
+                            cudaStream_t s);
 cudaError_t gemm_set_attributes();
 
 // setup (float64, device)

@@ -57,11 +57,12 @@ __device__ __forceinline__ int bitrev_r(int i) {
 // Complex H = 32R point FFT of z[n'] = x[2n'] + j x[2n'+1] as 32R = R x 32 (pass 1: R-point DFTs over r in
 // registers, twiddle, transpose through padded smem; pass 2: the 32-point DFTs over the lane index split as
 // R-point in registers x G = 32/R across lanes).  Then the real-FFT post pass, PHAT, FP16 records.
-template <int R>
+template <int R, int BPC>
 __global__ void __launch_bounds__(32 * STFT_WARPS)
     stft_phat_kernel(const float* __restrict__ audio, int64_t cs, int64_t fstride, int F, int Mi, int64_t F_pad,
                      const float* __restrict__ win, const float2* __restrict__ twN, uint8_t* __restrict__ P16,
-                     int bpc, int n_chunks) {
+                     int n_chunks) {
+    constexpr int bpc = BPC;
     constexpr int N = 64 * R;
     constexpr int H = N / 2;
     constexpr int Kb = H + 1;
@@ -92,7 +93,7 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
 #pragma unroll
         for (int i = 0; i < R; ++i) {
             const int k1 = bitrev_r<R>(i);
-            wbuf[k1 * SROW + lane] = (k1 == 0) ? a[i] : cmul(a[i], __ldg(twN + ((2 * lane * k1) % N)));
+            wbuf[k1 * SROW + lane] = (k1 == 0) ? a[i] : cmul(a[i], __ldg(twN + ((2 * lane * k1) & (N - 1))));
         }
         __syncwarp();
         // pass 2: lane (k1 = lane / G, h = lane % G) takes l = G j + h, j < R
@@ -104,7 +105,7 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
 #pragma unroll
         for (int i = 0; i < R; ++i) {
             const int aa = bitrev_r<R>(i);
-            if (h * aa) a[i] = cmul(a[i], __ldg(twN + ((h * aa) * (N / 32)) % N));   // W_32^{h a}
+            if (h * aa) a[i] = cmul(a[i], __ldg(twN + (((h * aa) * (N / 32)) & (N - 1))));   // W_32^{h a}
 #pragma unroll
             for (int hh = G / 2; hh >= 1; hh >>= 1) {           // G-point DIF across the lane group
                 const float ox = __shfl_xor_sync(0xffffffffu, a[i].x, hh);
@@ -146,8 +147,8 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
             const float2 t = cmul(__ldg(twN + k), Dd);                                   // w^k (Z - Zr)/2
             e = phat(make_float2(E.x + t.y, E.y - t.x));                                // E - j t
         }
-        const int cc = k / bpc, s = k % bpc;
-        __half* rec = reinterpret_cast<__half*>(tile + cc * tile_stride + warp * (bpc * 4));
+        const int cc = k / BPC, s = k % BPC;
+        __half* rec = reinterpret_cast<__half*>(tile + cc * tile_stride + warp * (BPC * 4));
         rec[s] = __float2half_rn(e.x);
         rec[bpc + s] = __float2half_rn(e.y);
     }
@@ -209,22 +210,27 @@ __global__ void stft_phat_small_kernel(const float* __restrict__ audio, int64_t 
     }
 }
 
-template <int R>
-static cudaError_t launch_r(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F, cudaStream_t s) {
+template <int R, int BPC>
+static cudaError_t launch_rb(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F, cudaStream_t s) {
     const int H = 32 * R;
     const int wbuf = (R * 34 > H + H / 32 + 2) ? R * 34 : H + H / 32 + 2;
     const size_t smem = STFT_WARPS * wbuf * sizeof(float2) + (size_t)p.L.n_chunks * (STFT_WARPS * 16 + 16);
     static bool attr_done = false;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(stft_phat_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaError_t e = cudaFuncSetAttribute(stft_phat_kernel<R, BPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              200 * 1024);
         if (e != cudaSuccess) return e;
         attr_done = true;
     }
     dim3 grid((F + STFT_WARPS - 1) / STFT_WARPS, p.M);
-    stft_phat_kernel<R><<<grid, 32 * STFT_WARPS, smem, s>>>(audio, cs, fstride, F, p.L.Mi, p.F_pad, p.d_window,
-                                                            p.d_twN, p.d_P16, p.L.bpc, p.L.n_chunks);
+    stft_phat_kernel<R, BPC><<<grid, 32 * STFT_WARPS, smem, s>>>(audio, cs, fstride, F, p.L.Mi, p.F_pad, p.d_window,
+                                                                 p.d_twN, p.d_P16, p.L.n_chunks);
     return cudaGetLastError();
+}
+
+template <int R>
+static cudaError_t launch_r(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F, cudaStream_t s) {
+    return p.L.bpc == 4 ? launch_rb<R, 4>(p, audio, cs, fstride, F, s) : launch_rb<R, 2>(p, audio, cs, fstride, F, s);
 }
 
 cudaError_t launch_stft_phat(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F,

@@ -239,3 +239,94 @@ def test_small_random_arrays(M, N, level, field):
     P_, Y_at = PP.svd_reference(fac, tau, x[keep], N)
     PP.compare(q[F:][keep], s[F:][keep], P_, Y_at, f"M={M} N={N} SVD")
     plan.close()
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg,n_sub", [(3, 64), (4, 12)])
+def test_svd_full_size_against_oracle_svd(cfg, n_sub):
+    """Full-size SVD-PHAT parity: the oracle's own float64 SVD of W (Gram route, minutes on the host) vs the
+    device plan; D must agree exactly and the DOAs/scores must pass the parity rules on sampled frames."""
+    import time
+    w = make(cfg)
+    plan = _plan(w, methods=("svd",))
+    audio = torch.from_numpy(w.audio).to(DEV)
+    q, s = _run(plan, w, "svd", audio, w.n_frames)
+    tau = srp.tdoa(w.mics, w.points, w.fs, w.c, w.field)
+    t0 = time.time()
+    fac = svd.svd_factors(tau, w.N, w.delta, method="gram")
+    print(f"cfg{cfg}: oracle SVD {time.time() - t0:.0f}s, D oracle {fac['D']} plan {plan.info()['D']}")
+    assert plan.info()["D"] == fac["D"]
+    rng = np.random.default_rng(cfg + 100)
+    sub = np.sort(rng.choice(w.n_frames, n_sub, replace=False))
+    x = srp.frames_to_x(PP._frames_subset(w, sub))
+    P_, Y_at = PP.svd_reference(fac, tau, x, w.N)
+    print(PP.compare(q[sub], s[sub], P_, Y_at, f"cfg{cfg} SVD full size"))
+    plan.close()
+
+
+def test_full_rank_svd_equals_srp_on_gpu():
+    """GPU-internal invariant (any size): with D = the numerical rank, SVD-PHAT and SRP-PHAT return the same DOAs."""
+    w = make(5, 256)
+    tau = srp.tdoa(w.mics, w.points, w.fs, w.c, w.field)
+    plan0 = _plan(w, max_frames=256)
+    s2 = plan0.sigma2(plan0.info()["Q_classes"])
+    plan0.close()
+    full = int(np.sum(s2 > 1e-12 * s2[0]))
+    plan = _plan(w, max_frames=256, rank_D=full)
+    assert plan.info()["D"] == full
+    audio = torch.from_numpy(w.audio).to(DEV)
+    d = torch.empty(512, dtype=torch.int32, device=DEV)
+    sc = torch.empty(512, dtype=torch.float32, device=DEV)
+    plan.localize("both", audio, 256, w.channel_stride, w.frame_stride, d, sc, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    q = d.cpu().numpy()
+    agree = np.mean(q[:256] == q[256:])
+    assert agree >= 0.995, agree
+    plan.close()
+
+
+@pytest.mark.parametrize("cfg,frames", [(1, None), (3, 5000)])
+def test_host_buffer_path_matches_device_path(cfg, frames):
+    """svdphat_localize_host (pinned host buffers, chunked H2D overlapped with compute for frame-major batches)
+    returns exactly the device-path results."""
+    w = make(cfg, frames)
+    plan = _plan(w, max_frames=w.n_frames)
+    F = w.n_frames
+    audio = torch.from_numpy(w.audio).to(DEV)
+    d = torch.empty(2 * F, dtype=torch.int32, device=DEV)
+    sc = torch.empty(2 * F, dtype=torch.float32, device=DEV)
+    st = torch.cuda.current_stream().cuda_stream
+    plan.localize("both", audio, F, w.channel_stride, w.frame_stride, d, sc, st)
+    torch.cuda.synchronize()
+    h_audio = torch.from_numpy(w.audio).pin_memory()
+    hd = torch.empty(2 * F, dtype=torch.int32).pin_memory()
+    hs = torch.empty(2 * F, dtype=torch.float32).pin_memory()
+    plan.localize_host("both", h_audio, w.audio.size, F, w.channel_stride, w.frame_stride, hd, hs, st)
+    assert np.array_equal(hd.numpy(), d.cpu().numpy())
+    assert np.array_equal(hs.numpy(), sc.cpu().numpy())
+    plan.close()
+
+
+@pytest.mark.parametrize("name", ["1d", "2d", "3d"])
+def test_device_setup_reproduces_paper_rank_curve(name):
+    """Fig. 2b/2c: the device float64 setup (closed-form Gram + cuSOLVER) gives the paper's gains
+    320/53/36 at delta = 1e-5 (Table 1 + Table 2, tests/golden/) and the oracle's D(delta) over 1e-1..1e-6."""
+    import json
+    import os
+    from workloads import geometry as G
+    gold = os.path.join(os.path.dirname(__file__), "golden")
+    t1 = json.load(open(os.path.join(gold, "paper_table1.json")))
+    mics = np.asarray(json.load(open(os.path.join(gold, "paper_table2_cm.json")))[name]) / 100.0
+    gains = json.load(open(os.path.join(gold, "paper_gains.json")))
+    grid = G.icosphere(4)
+    plan = S.Plan(mics, grid, t1["fs"], t1["c"], t1["N"], t1["hop"], "far", delta=gains["delta"], methods=("svd",),
+                  max_frames=16)
+    D = plan.info()["D"]
+    assert round(t1["Q"] / D) == gains["gain"][name]
+    tau = srp.tdoa(mics, grid, t1["fs"], t1["c"], "far")
+    fac = svd.svd_factors(tau, t1["N"], gains["delta"], method="svd")
+    s2 = plan.sigma2(plan.info()["Q_classes"])
+    tot = plan.info()["trace_WWH"]
+    for delta in (1e-1, 1e-2, 1e-3, 1e-4, 1e-5, 1e-6):
+        assert svd.rank_rule(s2, tot, delta) == svd.rank_rule(fac["sigma2"], fac["total"], delta), delta
+    plan.close()
