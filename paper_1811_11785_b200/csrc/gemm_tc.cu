@@ -963,8 +963,8 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
     if (tiles == 0) return cudaSuccess;
     if (mode == 2) return launch_one<4, 4, 2>(*A, *B, gp, grid, s);
     static const int ts = [] {
-        const char* e = getenv("SVDPHAT_SRP_TS");
-        return e ? atoi(e) : 1;
+        const char* e = getenv("SVDPHAT_SRP_TS");   // TS variant: correct, but 3% slower at cfg3 (r01 ncu:
+        return e ? atoi(e) : 0;                    // tensor pipe 74% active although the MMA never waits)
     }();
     if (mode == 0 && p.pair_srp && ts) {
         gp.m_tiles = p.Q_pad / 256;
