@@ -128,6 +128,11 @@ struct svdphat_plan_s {
             if (p.ev_done[i]) cudaEventDestroy(p.ev_done[i]);
         }
         if (p.copy_stream) cudaStreamDestroy(p.copy_stream);
+        if (p.ev_fork) cudaEventDestroy(p.ev_fork);
+        if (p.ev_join) cudaEventDestroy(p.ev_join);
+        if (p.svd_stream) cudaStreamDestroy(p.svd_stream);
+        if (p.srp_stream) cudaStreamDestroy(p.srp_stream);
+        if (p.ev_join2) cudaEventDestroy(p.ev_join2);
         void* bufs[] = {p.d_W16, p.d_V16, p.d_R16, p.d_rep, p.d_delay, p.d_window, p.d_twN, p.d_P16,
                         p.d_keys, p.d_Z32, p.d_Zs16, p.d_zflag, p.d_stage, p.d_doa_stage, p.d_score_stage};
         for (void* b : bufs)
@@ -331,6 +336,15 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(Zs) failed");
     }
     SVD_CUDA_TRY(gemm_set_attributes());
+    if ((p.methods & SVDPHAT_METHOD_BOTH) == SVDPHAT_METHOD_BOTH) {
+        int lo = 0, hi = 0;
+        SVD_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+        SVD_CUDA_TRY(cudaStreamCreateWithPriority(&p.svd_stream, cudaStreamNonBlocking, lo));
+        SVD_CUDA_TRY(cudaStreamCreateWithPriority(&p.srp_stream, cudaStreamNonBlocking, hi));
+        SVD_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming));
+        SVD_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming));
+        SVD_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_join2, cudaEventDisableTiming));
+    }
     SVD_CUDA_TRY(cudaDeviceSynchronize());
     p.setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = h.release();
@@ -374,17 +388,31 @@ svdphat_status svdphat_plan_sigma2(svdphat_plan_t plan, double* out, int32_t n) 
 static svdphat_status localize_impl(Plan& p, int32_t method, const float* d_audio, int F, int64_t channel_stride,
                                     int64_t frame_stride, int32_t* doa_srp, float* sc_srp, int32_t* doa_svd,
                                     float* sc_svd, cudaStream_t s) {
+    // BOTH: after the STFT the SRP GEMM (high-priority stream) and the SVD chain (low-priority stream) run
+    // concurrently: the SRP CTAs take every SM first and the SVD kernels fill the SMs its last wave releases.
+    // Stage events are recorded on each kernel's own stream (an SVD stage's time may include waiting for SMs).
+    const bool fork = method == SVDPHAT_METHOD_BOTH && p.svd_stream;
+    cudaStream_t sr = fork ? p.srp_stream : s, sv = fork ? p.svd_stream : s;
+    SVD_CUDA_TRY(cudaMemsetAsync(p.d_keys, 0, (size_t)2 * p.F_pad * 8, s));
     SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_STFT, s,
                         [&] { return launch_stft_phat(p, d_audio, channel_stride, frame_stride, F, s); }));
-    if (method & SVDPHAT_METHOD_SRP) {
-        SVD_CUDA_TRY(cudaMemsetAsync(p.d_keys, 0, (size_t)F * 8, s));
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_GEMM, s, [&] { return launch_gemm(p, 0, F, s); }));
+    if (fork) {
+        SVD_CUDA_TRY(cudaEventRecord(p.ev_fork, s));
+        SVD_CUDA_TRY(cudaStreamWaitEvent(sr, p.ev_fork, 0));
+        SVD_CUDA_TRY(cudaStreamWaitEvent(sv, p.ev_fork, 0));
     }
+    if (method & SVDPHAT_METHOD_SRP)
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_GEMM, sr, [&] { return launch_gemm(p, 0, F, sr); }));
     if (method & SVDPHAT_METHOD_SVD) {
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_PROJ, s, [&] { return launch_gemm(p, 1, F, s); }));
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_NORM, s, [&] { return launch_zsplit(p, F, s); }));
-        SVD_CUDA_TRY(cudaMemsetAsync(p.d_keys + p.F_pad, 0, (size_t)F * 8, s));
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_SEARCH, s, [&] { return launch_gemm(p, 2, F, s); }));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_PROJ, sv, [&] { return launch_gemm(p, 1, F, sv); }));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_NORM, sv, [&] { return launch_zsplit(p, F, sv); }));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_SEARCH, sv, [&] { return launch_gemm(p, 2, F, sv); }));
+    }
+    if (fork) {
+        SVD_CUDA_TRY(cudaEventRecord(p.ev_join, sr));
+        SVD_CUDA_TRY(cudaEventRecord(p.ev_join2, sv));
+        SVD_CUDA_TRY(cudaStreamWaitEvent(s, p.ev_join, 0));
+        SVD_CUDA_TRY(cudaStreamWaitEvent(s, p.ev_join2, 0));
     }
     int32_t* const doas[2] = {doa_srp, doa_svd};
     float* const scores[2] = {sc_srp, sc_svd};

@@ -73,6 +73,11 @@ struct Plan {
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev_copied[2] = {nullptr, nullptr};
     cudaEvent_t ev_done[2] = {nullptr, nullptr};
+    // method BOTH: the SVD chain runs on svd_stream, forked after the STFT and joined before the finalize, so its
+    // kernels fill the SMs released by the SRP GEMM's last (partial) wave
+    cudaStream_t svd_stream = nullptr;   // lowest priority
+    cudaStream_t srp_stream = nullptr;   // highest priority: its CTAs are dispatched before the SVD chain's
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
     int32_t* d_doa_stage = nullptr;
     float* d_score_stage = nullptr;
     int64_t last_frames = 0;
