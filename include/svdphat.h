@@ -116,6 +116,18 @@ svdphat_status svdphat_localize_host(svdphat_plan_t plan, int32_t method, const 
                                      int64_t audio_elems, int64_t n_frames, int64_t channel_stride,
                                      int64_t frame_stride, int32_t* h_doa, float* h_score, void* stream);
 
+/* Multi-source extension (future work: "investigate multiple source localization").  For each frame,
+ * the k (1..4) strongest peaks of the method's power map — SRP: Y_q (eq. 5); SVD: Re{D_hat_q . Z_hat} (eq. 14) —
+ * taken greedily, each peak excluding all candidates whose direction is within min_sep_deg of a stronger peak
+ * (directions from the array centroid; steering classes of DESIGN.md R11 count as one candidate).
+ *   d_doa[f*k + j], d_score[f*k + j] (DEVICE): peak j of frame f (point index, Y_q of eq. 5), strongest first;
+ *   -1 / 0 when fewer than j+1 candidates remain or the frame is degenerate (R4).
+ * method SRP or SVD.  On first use allocates a float32 power-map workspace of max_frames x Q_classes (ALLOC on
+ * failure).  Q_classes must be <= 49152 (the map of one frame is staged in shared memory); INVALID_ARG otherwise. */
+svdphat_status svdphat_localize_topk(svdphat_plan_t plan, int32_t method, const float* d_audio, int64_t n_frames,
+                                     int64_t channel_stride, int64_t frame_stride, int32_t k, double min_sep_deg,
+                                     int32_t* d_doa, float* d_score, void* stream);
+
 /* Releases all device and host memory of the plan (NULL is a no-op).  The caller must have synchronised any
  * stream a localize was issued on. */
 void svdphat_plan_destroy(svdphat_plan_t plan);

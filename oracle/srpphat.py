@@ -169,3 +169,32 @@ def srp_localize(tau: np.ndarray, x: np.ndarray, N: int) -> tuple[np.ndarray, np
 def frames_to_x(frames: np.ndarray) -> np.ndarray:
     """Alg. 1 online step 1: frames (F, M, N) -> X vector (F, P*K)."""
     return cross_spectrum(stft(frames))
+
+
+# ---------------------------------------------------------------- multi-source extension (NEXT-1; P:452)
+def steering_classes(tau: np.ndarray) -> np.ndarray:
+    """Representative (lowest) point index of each set of identical steering rows (reading R11), ascending."""
+    _, first = np.unique(tau, axis=0, return_index=True)
+    return np.sort(first)
+
+
+def topk_peaks(P: np.ndarray, dirs: np.ndarray, reps: np.ndarray, k: int, sep_deg: float,
+               rel: float = 1e-9) -> np.ndarray:
+    """The paper names multiple-source localisation as future work without an algorithm; reading R21:
+    greedy peaks of the power map P (F, Q) over the steering classes `reps`, each round taking the best class not
+    within sep_deg of an earlier peak (unit directions `dirs`, from the array centroid), lowest index among near-ties.
+    Returns (F, k) point indices, -1 when no candidate is left."""
+    cs = np.cos(np.radians(sep_deg))
+    out = -np.ones((P.shape[0], k), dtype=np.int64)
+    D = dirs[reps]
+    for f in range(P.shape[0]):
+        alive = np.ones(len(reps), dtype=bool)
+        for j in range(k):
+            if not alive.any():
+                break
+            v = np.where(alive, P[f, reps], -np.inf)
+            best = v.max()
+            c = int(np.argmax(alive & (v >= best - rel * abs(best))))
+            out[f, j] = reps[c]
+            alive &= (D @ D[c]) < cs
+    return out

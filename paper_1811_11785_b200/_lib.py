@@ -53,6 +53,7 @@ def _load() -> C.CDLL:
         "svdphat_last_error": (C.c_char_p, []),
         "svdphat_debug_dump": (st, [vp, i32, i64, vp, i64]),
         "svdphat_profile_begin": (st, [vp, i32]),
+        "svdphat_localize_topk": (st, [vp, i32, vp, i64, i64, i64, i32, C.c_double, vp, vp, vp]),
         "svdphat_profile_end": (i32, [vp, C.POINTER(i32), C.POINTER(C.c_float), i32]),
     }
     for name, (res, args) in sig.items():
@@ -132,6 +133,14 @@ class Plan:
         _check(lib.svdphat_localize_host(self._h, _METHOD[method], _ptr(audio),
                                          audio_elems, n_frames, channel_stride, frame_stride, _ptr(doa), _ptr(score),
                                          stream), "svdphat_localize_host")
+
+    def localize_topk(self, method: str, audio, n_frames: int, channel_stride: int, frame_stride: int, k: int,
+                      min_sep_deg: float, doa, score, stream: int = 0) -> None:
+        """Multi-source: the k strongest peaks per frame (doa/score: CUDA tensors of n_frames*k), separated by at
+        least min_sep_deg; method "srp" or "svd"."""
+        _check(lib.svdphat_localize_topk(self._h, _METHOD[method], _ptr(audio), n_frames, channel_stride,
+                                         frame_stride, k, min_sep_deg, _ptr(doa), _ptr(score), stream),
+               "svdphat_localize_topk")
 
     def profile_begin(self, capacity: int) -> None:
         _check(lib.svdphat_profile_begin(self._h, capacity), "profile_begin")

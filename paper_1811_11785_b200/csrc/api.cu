@@ -133,8 +133,9 @@ struct svdphat_plan_s {
         if (p.svd_stream) cudaStreamDestroy(p.svd_stream);
         if (p.srp_stream) cudaStreamDestroy(p.srp_stream);
         if (p.ev_join2) cudaEventDestroy(p.ev_join2);
-        void* bufs[] = {p.d_W16, p.d_V16, p.d_R16, p.d_rep, p.d_delay, p.d_window, p.d_twN, p.d_P16,
-                        p.d_keys, p.d_Z32, p.d_Zs16, p.d_zflag, p.d_stage, p.d_doa_stage, p.d_score_stage};
+        void* bufs[] = {p.d_W16,   p.d_V16,   p.d_R16,   p.d_rep,   p.d_delay,     p.d_window,      p.d_twN,
+                        p.d_P16,   p.d_keys,  p.d_Z32,   p.d_Zs16,  p.d_zflag,     p.d_stage,       p.d_doa_stage,
+                        p.d_score_stage, p.d_S, p.d_cls, p.d_dirs};
         for (void* b : bufs)
             if (b) cudaFree(b);
     }
@@ -286,6 +287,30 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
         std::vector<float> df(delay.begin(), delay.end());
         SVD_CUDA_TRY(cudaMalloc(&p.d_delay, df.size() * sizeof(float)));
         SVD_CUDA_TRY(cudaMemcpy(p.d_delay, df.data(), df.size() * sizeof(float), cudaMemcpyHostToDevice));
+    }
+    {
+        // unit direction of each class representative as seen from the array centroid (multi-source suppression)
+        double cx = 0, cy = 0, cz = 0;
+        for (int m = 0; m < M; ++m) {
+            cx += r[3 * m] / M;
+            cy += r[3 * m + 1] / M;
+            cz += r[3 * m + 2] / M;
+        }
+        std::vector<float4> dirs(p.Q_eff);
+        for (int c = 0; c < p.Q_eff; ++c) {
+            const double* s = d->points_xyz + 3 * (size_t)p.rep_q[c];
+            double v[3] = {s[0], s[1], s[2]};
+            if (p.field == SVDPHAT_FIELD_NEAR) {
+                v[0] -= cx;
+                v[1] -= cy;
+                v[2] -= cz;
+            }
+            const double n = std::sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+            dirs[c] = n > 0 ? make_float4((float)(v[0] / n), (float)(v[1] / n), (float)(v[2] / n), 0.f)
+                            : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+        SVD_CUDA_TRY(cudaMalloc(&p.d_dirs, dirs.size() * sizeof(float4)));
+        SVD_CUDA_TRY(cudaMemcpy(p.d_dirs, dirs.data(), dirs.size() * sizeof(float4), cudaMemcpyHostToDevice));
     }
     {
         std::vector<float> w(p.N);
@@ -446,6 +471,45 @@ svdphat_status svdphat_localize(svdphat_plan_t plan, int32_t method, const float
     const bool both = method == SVDPHAT_METHOD_BOTH;
     return localize_impl(p, method, d_audio, F, channel_stride, frame_stride, d_doa, d_score,
                          both ? d_doa + F : d_doa, both ? d_score + F : d_score, reinterpret_cast<cudaStream_t>(stream));
+}
+
+svdphat_status svdphat_localize_topk(svdphat_plan_t plan, int32_t method, const float* d_audio, int64_t n_frames,
+                                     int64_t channel_stride, int64_t frame_stride, int32_t k, double min_sep_deg,
+                                     int32_t* d_doa, float* d_score, void* stream) {
+    if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
+    Plan& p = plan->p;
+    if (method != SVDPHAT_METHOD_SRP && method != SVDPHAT_METHOD_SVD)
+        return fail(SVDPHAT_INVALID_ARG, "top-k: method must be SRP or SVD");
+    svdphat_status st = check_localize_args(p, method, n_frames, channel_stride, frame_stride);
+    if (st != SVDPHAT_OK) return st;
+    if (k < 1 || k > 4) return fail(SVDPHAT_INVALID_ARG, "k must be in [1, 4]");
+    if (!(min_sep_deg >= 0.0 && min_sep_deg <= 180.0)) return fail(SVDPHAT_INVALID_ARG, "min_sep_deg in [0, 180]");
+    if (p.Q_eff > 49152) return fail(SVDPHAT_INVALID_ARG, "top-k needs Q_classes <= 49152");
+    if (n_frames == 0) return SVDPHAT_OK;
+    if (!d_audio || !d_doa || !d_score) return fail(SVDPHAT_INVALID_ARG, "NULL buffer");
+    SVD_CUDA_TRY(cudaSetDevice(p.device));
+    if (!p.d_S) {
+        if (cudaMalloc(&p.d_S, (size_t)p.F_pad * p.Q_pad * sizeof(float)) != cudaSuccess ||
+            cudaMalloc(&p.d_cls, (size_t)p.F_pad * 4 * sizeof(int)) != cudaSuccess)
+            return fail(SVDPHAT_ALLOC, "top-k workspace allocation failed");
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int F = (int)n_frames;
+    SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_STFT, s,
+                        [&] { return launch_stft_phat(p, d_audio, channel_stride, frame_stride, F, s); }));
+    if (method == SVDPHAT_METHOD_SRP) {
+        SVD_CUDA_TRY(launch_gemm(p, 3, F, s));
+    } else {
+        SVD_CUDA_TRY(launch_gemm(p, 1, F, s));
+        SVD_CUDA_TRY(launch_zsplit(p, F, s));
+        SVD_CUDA_TRY(launch_gemm(p, 4, F, s));
+    }
+    const double kPi = 3.14159265358979323846;
+    SVD_CUDA_TRY(launch_topk(p, F, k, (float)std::cos(min_sep_deg * kPi / 180.0), s));
+    SVD_CUDA_TRY(launch_finalize_topk(p, F, k, d_doa, d_score, s));
+    p.last_frames = F;
+    p.last_method = method;
+    return SVDPHAT_OK;
 }
 
 svdphat_status svdphat_profile_begin(svdphat_plan_t plan, int32_t capacity) {

@@ -51,16 +51,20 @@ constexpr int FIN_WARPS = 8;
 // One or two methods per launch: method slot j in [0, nm) reads keys[j] and writes doa[j]/score[j]; the phasor
 // records of the frame are read once for both.
 struct FinOut {
-    const unsigned long long* keys[2];
-    const int* zflag[2];
-    int32_t* doa[2];
-    float* score[2];
+    const unsigned long long* keys[4];   // argmax path: keys[j][f]; nullptr -> class-list path
+    const int* cls;                      // class-list path: cls[f * cls_stride + j]
+    int cls_stride;
+    const int* zflag[4];
+    int32_t* doa[4];                     // output j of frame f at doa[j][f * out_stride]
+    float* score[4];
+    int out_stride;
 };
 
 template <int NM>
 __global__ void __launch_bounds__(32 * FIN_WARPS)
     finalize_kernel(FinOut o, const uint8_t* __restrict__ P16, int F, int64_t F_pad, int M, int Mi, int bpc,
                     int n_chunks, int Kb, int N, const int* __restrict__ rep, const float* __restrict__ delay) {
+    static_assert(NM >= 1 && NM <= 4, "1..4 results per frame");
     __shared__ float s_y[NM][FIN_WARPS][32];
     __shared__ int s_p[FIN_WARPS][32];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -70,8 +74,13 @@ __global__ void __launch_bounds__(32 * FIN_WARPS)
     const float* dq[NM];
 #pragma unroll
     for (int j = 0; j < NM; ++j) {
-        const unsigned long long key = valid ? o.keys[j][f] : 0ull;
-        const int cls = key ? (int)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull)) : -1;
+        int cls = -1;
+        if (o.keys[j]) {
+            const unsigned long long key = valid ? o.keys[j][f] : 0ull;
+            cls = key ? (int)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFull)) : -1;
+        } else if (valid) {
+            cls = o.cls[(int64_t)f * o.cls_stride + j];
+        }
         q[j] = cls >= 0 ? rep[cls] : -1;
         dq[j] = delay + (int64_t)(q[j] >= 0 ? q[j] : 0) * M;
     }
@@ -154,8 +163,8 @@ __global__ void __launch_bounds__(32 * FIN_WARPS)
 #pragma unroll
             for (int w = 0; w < FIN_WARPS; ++w) y += s_y[j][w][lane];
             const bool dead = (pr == 0) || q[j] < 0 || (o.zflag[j] != nullptr && o.zflag[j][f] != 0);
-            o.doa[j][f] = dead ? -1 : q[j];
-            o.score[j][f] = dead ? 0.f : 0.5f * y;
+            o.doa[j][(int64_t)f * o.out_stride] = dead ? -1 : q[j];
+            o.score[j][(int64_t)f * o.out_stride] = dead ? 0.f : 0.5f * y;
         }
     }
 }
@@ -174,6 +183,7 @@ cudaError_t launch_finalize(const Plan& p, int method, int F, int32_t* const doa
                             cudaStream_t s) {
     if (F <= 0) return cudaSuccess;
     FinOut o{};
+    o.out_stride = 1;
     int nm = 0;
     if (method & SVDPHAT_METHOD_SRP) {
         o.keys[nm] = p.d_keys;
@@ -196,6 +206,108 @@ cudaError_t launch_finalize(const Plan& p, int method, int F, int32_t* const doa
     else
         finalize_kernel<1><<<grid, block, 0, s>>>(o, p.d_P16, F, p.F_pad, p.M, p.L.Mi, p.L.bpc, p.L.n_chunks, p.Kb,
                                                   p.N, p.d_rep, p.d_delay);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_finalize_topk(const Plan& p, int F, int k, int32_t* doa, float* score, cudaStream_t s) {
+    if (F <= 0) return cudaSuccess;
+    FinOut o{};
+    o.cls = p.d_cls;
+    o.cls_stride = 4;
+    o.out_stride = k;
+    for (int j = 0; j < k; ++j) {
+        o.keys[j] = nullptr;
+        o.zflag[j] = nullptr;
+        o.doa[j] = doa + j;
+        o.score[j] = score + j;
+    }
+    const dim3 grid((F + 31) / 32), block(32 * FIN_WARPS);
+#define SVD_FIN(K)                                                                                                 \
+    if (k == K) {                                                                                                  \
+        finalize_kernel<K><<<grid, block, 0, s>>>(o, p.d_P16, F, p.F_pad, p.M, p.L.Mi, p.L.bpc, p.L.n_chunks, p.Kb,  \
+                                                  p.N, p.d_rep, p.d_delay);                                        \
+        return cudaGetLastError();                                                                                 \
+    }
+    SVD_FIN(1)
+    SVD_FIN(2)
+    SVD_FIN(3)
+    SVD_FIN(4)
+#undef SVD_FIN
+    return cudaErrorInvalidValue;
+}
+
+// ---------------------------------------------------------------- multi-source peak picking
+// CTA per frame: the frame's power map (one value per steering class) is staged in shared memory; k rounds of a
+// block-wide argmax (lowest class on ties) skipping classes within the suppression cone (dot >= cos_sep) of the
+// peaks already taken.
+__global__ void __launch_bounds__(256)
+    topk_kernel(const float* __restrict__ S, int ldS, int Q, int F, const float4* __restrict__ dirs, int k,
+                float cos_sep, int* __restrict__ cls_out) {
+    extern __shared__ float sc[];
+    __shared__ float s_v[8];
+    __shared__ int s_i[8];
+    __shared__ float4 sel[4];
+    const int f = blockIdx.x;
+    if (f >= F) return;
+    const float* row = S + (int64_t)f * ldS;
+    for (int q = threadIdx.x; q < Q; q += blockDim.x) sc[q] = row[q];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int j = 0; j < k; ++j) {
+        float bv = -INFINITY;
+        int bi = 0x7FFFFFFF;
+        for (int q = threadIdx.x; q < Q; q += blockDim.x) {
+            const float v = sc[q];
+            if (!(v > bv || (v == bv && q < bi))) continue;
+            const float4 d = __ldg(dirs + q);
+            bool sup = false;
+            for (int i = 0; i < j; ++i) sup |= (d.x * sel[i].x + d.y * sel[i].y + d.z * sel[i].z) >= cos_sep;
+            if (!sup) {
+                bv = v;
+                bi = q;
+            }
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) {
+            const float ov = __shfl_xor_sync(0xffffffffu, bv, o);
+            const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+            if (ov > bv || (ov == bv && oi < bi)) {
+                bv = ov;
+                bi = oi;
+            }
+        }
+        if (lane == 0) {
+            s_v[warp] = bv;
+            s_i[warp] = bi;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float v = s_v[0];
+            int i = s_i[0];
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
+                if (s_v[w] > v || (s_v[w] == v && s_i[w] < i)) {
+                    v = s_v[w];
+                    i = s_i[w];
+                }
+            const bool ok = i != 0x7FFFFFFF && v > -INFINITY;
+            cls_out[(int64_t)f * 4 + j] = ok ? i : -1;
+            sel[j] = ok ? dirs[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+            if (!ok) sel[j].x = 2.0f;             // no further peak: suppress nothing, later rounds also empty
+        }
+        __syncthreads();
+    }
+}
+
+cudaError_t launch_topk(const Plan& p, int F, int k, float cos_sep, cudaStream_t s) {
+    if (F <= 0) return cudaSuccess;
+    const size_t smem = (size_t)p.Q_eff * sizeof(float);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+        cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+        attr = smem;
+    }
+    topk_kernel<<<F, 256, smem, s>>>(p.d_S, p.Q_pad, p.Q_eff, F, p.d_dirs, k, cos_sep, p.d_cls);
     return cudaGetLastError();
 }
 

@@ -117,7 +117,8 @@ __device__ __forceinline__ unsigned long long transpose_max32(unsigned long long
 template <int Mi, int BPC, int MODE>
 __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
-    constexpr bool kProducer = (MODE != 2);
+    // MODE 0: producer B + argmax, 1: producer B + store, 2: TMA B + argmax, 3: TMA B + store
+    constexpr bool kProducer = (MODE == 0 || MODE == 1);
     constexpr int kPairs = Mi * (Mi - 1) / 2;
     constexpr int kUnitsRaw = (BPC == 4) ? kPairs : (kPairs + 1) / 2;
     constexpr int kU = (kUnitsRaw + 7) / 8 * 8;        // units per chunk
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
                 tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + acc * BN + j0, r);
                 tmem_ld_wait();
                 const int f0 = n * BN + j0;
-                if (MODE == 1) {
+                if (MODE == 1 || MODE == 3) {
                     if (row_ok) {
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj) {
@@ -882,6 +883,11 @@ cudaError_t gemm_set_attributes() {
     SVD_ATTR(16, 4)
     SVD_ATTR(32, 2)
 #undef SVD_ATTR
+    if ((e = set_attr_one<4, 4, 3>()) != cudaSuccess) return e;
+    if ((e = set_attr_two<4, 4, 1>()) != cudaSuccess) return e;
+    if ((e = set_attr_two<8, 4, 1>()) != cudaSuccess) return e;
+    if ((e = set_attr_two<16, 4, 1>()) != cudaSuccess) return e;
+    if ((e = set_attr_two<32, 2, 1>()) != cudaSuccess) return e;
     return set_attr_one<4, 4, 2>();
 }
 
@@ -945,13 +951,44 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
         gp.n_slabs = (int)(p.L.K_total / BK);
         gp.m_tiles = (2 * p.Dh) / BM;
         gp.rows_valid = 2 * p.Dh;
-    } else {
+    } else if (mode == 2) {
         A = &p.tm_R;
         B = &p.tm_Zs;
         gp.keys = p.d_keys + p.F_pad;
         gp.n_slabs = p.K2 / BK;
         gp.m_tiles = p.Q_pad / BM;
         gp.rows_valid = p.Q_eff;
+    } else if (mode == 3) {            // SRP power map Y[f][class] -> S (multi-source search)
+        A = &p.tm_W;
+        gp.n_slabs = (int)(p.L.K_total / BK);
+        gp.rows_valid = p.Q_eff;
+        gp.Z = p.d_S;
+        gp.ldz = p.Q_pad;
+    } else {                           // mode 4: SVD search power map Re{Dhat Zhat}[f][class] -> S
+        A = &p.tm_R;
+        B = &p.tm_Zs;
+        gp.n_slabs = p.K2 / BK;
+        gp.m_tiles = p.Q_pad / BM;
+        gp.rows_valid = p.Q_eff;
+        gp.Z = p.d_S;
+        gp.ldz = p.Q_pad;
+    }
+    if (mode == 3) {
+        gp.m_tiles = p.Q_pad / 256;
+        const int units = gp.m_tiles * gp.n_tiles;
+        const int pairs = units < p.num_sms / 2 ? units : p.num_sms / 2;
+        if (units == 0) return cudaSuccess;
+#define SVD_DISPATCH4(MI, BP)                                                                  \
+    if (p.L.Mi == MI) {                                                                       \
+        gemm2_kernel<MI, BP, 1><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(*A, *B, gp);          \
+        return cudaGetLastError();                                                            \
+    }
+        SVD_DISPATCH4(4, 4)
+        SVD_DISPATCH4(8, 4)
+        SVD_DISPATCH4(16, 4)
+        SVD_DISPATCH4(32, 2)
+#undef SVD_DISPATCH4
+        return cudaErrorInvalidValue;
     }
     int tiles = gp.m_tiles * gp.n_tiles;
     if (mode == 1) {
@@ -962,6 +999,7 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
     const int grid = tiles < p.num_sms ? tiles : p.num_sms;
     if (tiles == 0) return cudaSuccess;
     if (mode == 2) return launch_one<4, 4, 2>(*A, *B, gp, grid, s);
+    if (mode == 4) return launch_one<4, 4, 3>(*A, *B, gp, grid, s);
     static const int ts = [] {
         const char* e = getenv("SVDPHAT_SRP_TS");   // TS variant: correct, but 3% slower at cfg3 (r01 ncu:
         return e ? atoi(e) : 0;                    // tensor pipe 74% active although the MMA never waits)

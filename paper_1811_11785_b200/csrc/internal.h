@@ -59,6 +59,10 @@ struct Plan {
     float* d_Z32 = nullptr;       // [MAX_KSPLIT][F_pad][2*Dh] partial Z of the split-K projection
     __half* d_Zs16 = nullptr;     // [F_pad][K2]
     int* d_zflag = nullptr;       // [F_pad]
+    // multi-source (top-k) workspace, allocated on first use: power map S[F_pad][Q_pad], class lists [F_pad][4]
+    float* d_S = nullptr;
+    int* d_cls = nullptr;
+    float4* d_dirs = nullptr;     // [Q_eff] unit direction of each class representative (from the array centroid)
     int64_t bytes_W = 0, bytes_V = 0, bytes_R = 0, bytes_ws = 0;
     // TMA descriptors
     alignas(64) CUtensorMap tm_W;
@@ -105,7 +109,7 @@ void set_error(const std::string& msg);
 cudaError_t launch_stft_phat(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F,
                              cudaStream_t s);
 // mode: 0 = SRP argmax (A = W16, B = producer), 1 = SVD GEMM1 store Z (A = V16, B = producer),
-//       2 = SVD search argmax (A = R16, B = Zs16 via TMA)
+//       2 = SVD search argmax (A = R16, B = Zs16 via TMA), 3 = SRP power map -> d_S, 4 = SVD search power map -> d_S
 cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s);
 cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s);
 constexpr int MAX_KSPLIT = 4;
@@ -113,6 +117,9 @@ int ksplit_for(const Plan& p, int tiles);   // K splits of the SVD projection GE
 // method SRP|SVD|BOTH; doa[0]/score[0] receive SRP results, doa[1]/score[1] SVD results
 cudaError_t launch_finalize(const Plan& p, int method, int F, int32_t* const doa[2], float* const score[2],
                             cudaStream_t s);
+// multi-source: greedy top-k with angular suppression over d_S -> class lists, then Y_q of each peak
+cudaError_t launch_topk(const Plan& p, int F, int k, float cos_sep, cudaStream_t s);
+cudaError_t launch_finalize_topk(const Plan& p, int F, int k, int32_t* doa, float* score, cudaStream_t s);
 cudaError_t gemm_set_attributes();
 
 // setup (float64, device)

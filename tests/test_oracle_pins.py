@@ -319,3 +319,37 @@ def test_kdtree_singleton_and_self_query():
     t = KDTree(pts)
     for i in range(100):
         assert t.nearest(pts[i]) == (i, 0.0)
+
+
+def test_topk_two_sources_injection():
+    """Two noiseless plane waves from grid points far apart -> the two strongest separated peaks are those points;
+    k = 1 equals the plain argmax."""
+    mics, grid, tau, N = _small_case(3, 256, "3d")
+    rng = np.random.default_rng(14)
+    reps = srp.steering_classes(tau)
+    assert len(reps) == len(grid)                       # 3-D array: no twins
+    frames, truth = [], []
+    for _ in range(6):
+        while True:
+            a, b = rng.choice(len(grid), 2, replace=False)
+            if np.degrees(np.arccos(grid[a] @ grid[b])) > 110:
+                break
+        sig = S.plane_wave_stream(rng, mics, FS, C, N, grid[a], 300.0) + \
+            S.plane_wave_stream(rng, mics, FS, C, N, grid[b], 300.0)
+        frames.append(sig)
+        truth.append({int(a), int(b)})
+    x = srp.frames_to_x(np.stack(frames))
+    Y = srp.srp_energy(tau, x, N)
+    top = srp.topk_peaks(Y, grid, reps, 2, 60.0)     # 10 cm aperture: broad main lobes (P:235-255)
+    for f in range(len(truth)):                         # each source within one level-3 grid spacing (~8 deg)
+        for t in truth[f]:
+            assert min(np.degrees(np.arccos(np.clip(grid[q] @ grid[t], -1, 1))) for q in top[f]) < 10.0
+    q1, _ = srp.argmax_tie(Y)
+    assert list(srp.topk_peaks(Y, grid, reps, 1, 25.0)[:, 0]) == list(q1)
+
+
+def test_steering_classes_planar():
+    mics, grid, tau, N = _small_case(2, 64, "2d")
+    reps = srp.steering_classes(tau)
+    mirror = np.array([int(np.argmin(np.linalg.norm(grid - g * [1, 1, -1], axis=1))) for g in grid])
+    assert sorted(reps.tolist()) == sorted(set(np.minimum(np.arange(len(grid)), mirror).tolist()))
