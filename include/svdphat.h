@@ -128,6 +128,17 @@ svdphat_status svdphat_localize_topk(svdphat_plan_t plan, int32_t method, const 
                                      int64_t channel_stride, int64_t frame_stride, int32_t k, double min_sep_deg,
                                      int32_t* d_doa, float* d_score, void* stream);
 
+/* Binary time-frequency masks (future work: "binary time-frequency mask, which could reduce even more
+ * the amount of computations").  As svdphat_localize, but bin k of frame l enters the X vector (eq. 7) only if
+ * k_lo <= k < k_hi and (d_mask == NULL or d_mask[l*mask_stride + k] != 0); excluded entries of eq. 3 are 0.  The band
+ * [k_lo, k_hi) is skipped at bin-chunk granularity by the projection GEMMs (compute ~ (k_hi-k_lo)/(N/2+1)); the
+ * DEVICE per-frame mask (uint8, mask_stride 0 = one row for all frames) changes the result, not the work.
+ * 0 <= k_lo < k_hi <= N/2+1, else INVALID_ARG. */
+svdphat_status svdphat_localize_masked(svdphat_plan_t plan, int32_t method, const float* d_audio, int64_t n_frames,
+                                       int64_t channel_stride, int64_t frame_stride, int32_t k_lo, int32_t k_hi,
+                                       const uint8_t* d_mask, int64_t mask_stride, int32_t* d_doa, float* d_score,
+                                       void* stream);
+
 /* Releases all device and host memory of the plan (NULL is a no-op).  The caller must have synchronised any
  * stream a localize was issued on. */
 void svdphat_plan_destroy(svdphat_plan_t plan);

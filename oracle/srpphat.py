@@ -198,3 +198,10 @@ def topk_peaks(P: np.ndarray, dirs: np.ndarray, reps: np.ndarray, k: int, sep_de
             out[f, j] = reps[c]
             alive &= (D @ D[c]) < cs
     return out
+
+
+def apply_tf_mask(x: np.ndarray, P: int, keep: np.ndarray) -> np.ndarray:
+    """Binary time-frequency mask (NEXT-3): X entries (eq. 7) of excluded bins are 0.
+    x (F, P*K), keep (F, K) bool -> masked copy of x."""
+    F = x.shape[0]
+    return (x.reshape(F, P, -1) * keep[:, None, :]).reshape(F, -1)

@@ -54,6 +54,7 @@ def _load() -> C.CDLL:
         "svdphat_debug_dump": (st, [vp, i32, i64, vp, i64]),
         "svdphat_profile_begin": (st, [vp, i32]),
         "svdphat_localize_topk": (st, [vp, i32, vp, i64, i64, i64, i32, C.c_double, vp, vp, vp]),
+        "svdphat_localize_masked": (st, [vp, i32, vp, i64, i64, i64, i32, i32, vp, i64, vp, vp, vp]),
         "svdphat_profile_end": (i32, [vp, C.POINTER(i32), C.POINTER(C.c_float), i32]),
     }
     for name, (res, args) in sig.items():
@@ -141,6 +142,13 @@ class Plan:
         _check(lib.svdphat_localize_topk(self._h, _METHOD[method], _ptr(audio), n_frames, channel_stride,
                                          frame_stride, k, min_sep_deg, _ptr(doa), _ptr(score), stream),
                "svdphat_localize_topk")
+
+    def localize_masked(self, method: str, audio, n_frames: int, channel_stride: int, frame_stride: int, k_lo: int,
+                        k_hi: int, mask, mask_stride: int, doa, score, stream: int = 0) -> None:
+        """Band limit [k_lo, k_hi) (skipped by the GEMMs) + optional per-frame binary TF mask (uint8 CUDA tensor)."""
+        _check(lib.svdphat_localize_masked(self._h, _METHOD[method], _ptr(audio), n_frames, channel_stride,
+                                           frame_stride, k_lo, k_hi, _ptr(mask), mask_stride, _ptr(doa), _ptr(score),
+                                           stream), "svdphat_localize_masked")
 
     def profile_begin(self, capacity: int) -> None:
         _check(lib.svdphat_profile_begin(self._h, capacity), "profile_begin")

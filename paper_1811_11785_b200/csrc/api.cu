@@ -204,6 +204,7 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     p.max_frames = d->max_frames;
     p.F_pad = std::max<int64_t>(256, (d->max_frames + 255) / 256 * 256);
     p.L = make_layout(d->M, d->N);
+    set_band(p, 0, p.Kb, nullptr, 0);
     p.trace = (double)p.Q * (double)p.P * (double)p.Kb;  // Tr{W W^H}, every |W| = 1 (eq. 4)
     p.num_sms = prop.multiProcessorCount;
 
@@ -471,6 +472,21 @@ svdphat_status svdphat_localize(svdphat_plan_t plan, int32_t method, const float
     const bool both = method == SVDPHAT_METHOD_BOTH;
     return localize_impl(p, method, d_audio, F, channel_stride, frame_stride, d_doa, d_score,
                          both ? d_doa + F : d_doa, both ? d_score + F : d_score, reinterpret_cast<cudaStream_t>(stream));
+}
+
+svdphat_status svdphat_localize_masked(svdphat_plan_t plan, int32_t method, const float* d_audio, int64_t n_frames,
+                                       int64_t channel_stride, int64_t frame_stride, int32_t k_lo, int32_t k_hi,
+                                       const uint8_t* d_mask, int64_t mask_stride, int32_t* d_doa, float* d_score,
+                                       void* stream) {
+    if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
+    Plan& p = plan->p;
+    if (k_lo < 0 || k_hi > p.Kb || k_lo >= k_hi) return fail(SVDPHAT_INVALID_ARG, "need 0 <= k_lo < k_hi <= N/2+1");
+    if (mask_stride < 0) return fail(SVDPHAT_INVALID_ARG, "negative mask_stride");
+    set_band(p, k_lo, k_hi, d_mask, mask_stride);
+    const svdphat_status st = svdphat_localize(plan, method, d_audio, n_frames, channel_stride, frame_stride, d_doa,
+                                               d_score, stream);
+    set_band(p, 0, p.Kb, nullptr, 0);
+    return st;
 }
 
 svdphat_status svdphat_localize_topk(svdphat_plan_t plan, int32_t method, const float* d_audio, int64_t n_frames,

@@ -173,7 +173,7 @@ cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s) {
     if (F <= 0) return cudaSuccess;
     const int threads = 256;
     const int blocks = (F * 32 + threads - 1) / threads;
-    const int tiles = (2 * p.Dh / 128) * ((F + 255) / 256);
+    const int tiles = (2 * p.Dh / 128) * ((F + 255) / 256);     // same split choice as the projection GEMM
     zsplit_kernel<<<blocks, threads, 0, s>>>(p.d_Z32, F, p.F_pad, 2 * p.Dh, ksplit_for(p, tiles), p.d_Zs16, p.K2,
                                              p.d_zflag);
     return cudaGetLastError();

@@ -44,6 +44,7 @@ struct GemmParams {
     int spc;                               // slabs per chunk
     int prefetch;                          // 0 none, 1 L2 prefetch of the next chunk's phasors, 2 same evict_last
     int bn;                                // frames per tile of the CTA-pair kernel (multiple of 32, <= 256)
+    int c_lo, c_hi;                        // active bin-chunk range (band limit, NEXT-3); producer modes only
     int dbg;                               // timing experiments only (SVDPHAT_GEMM_DBG): 1 producer writes zeros,
                                            // 2 TMA re-loads one W tile (results invalid)
 };
@@ -58,14 +59,14 @@ __device__ __forceinline__ Unit unit_of(const GemmParams& p, int t) {
     const int tile = t / p.ksplit;
     u.m = tile / p.n_tiles;
     u.n = tile % p.n_tiles;
-    if (p.ksplit == 1) {
-        u.c0 = 0;
-        u.c1 = p.n_chunks;
+    if (p.c_hi <= p.c_lo) {                // TMA-B modes: the whole contraction
+        u.c0 = u.c1 = 0;
         u.k0 = 0;
         u.k1 = p.n_slabs;
-    } else {
-        u.c0 = (int)((int64_t)u.s * p.n_chunks / p.ksplit);
-        u.c1 = (int)((int64_t)(u.s + 1) * p.n_chunks / p.ksplit);
+    } else {                               // producer modes: chunk range [c_lo, c_hi) split ksplit ways
+        const int nc = p.c_hi - p.c_lo;
+        u.c0 = p.c_lo + (int)((int64_t)u.s * nc / p.ksplit);
+        u.c1 = p.c_lo + (int)((int64_t)(u.s + 1) * nc / p.ksplit);
         u.k0 = u.c0 * p.spc;
         u.k1 = u.c1 * p.spc;
     }
@@ -684,7 +685,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS3, 1)
             uint32_t phase = 0;
             for (int t = pair; t < units; t += n_pairs) {
                 const int m = t / p.n_tiles;
-                for (int ks = 0; ks < p.n_slabs; ++ks) {
+                for (int ks = p.c_lo * p.spc; ks < p.c_hi * p.spc; ++ks) {
                     mbar_wait(&wempty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&wfull[stage], 2 * W3_BYTES);
                     tma_load_2d_2sm(sW + stage * W3_BYTES, &tmW, ks * BK, m * 256 + (int)rank * 128, &wfull[stage]);
@@ -703,7 +704,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS3, 1)
                 mbar_wait(tempty, tph ^ 1);
                 tph ^= 1;
                 tc_fence_after();
-                for (int ks = 0; ks < p.n_slabs; ++ks) {
+                for (int ks = p.c_lo * p.spc; ks < p.c_hi * p.spc; ++ks) {
                     mbar_wait(&wfull[ws], wph);
                     mbar_wait(&xfull[xs], xph);
                     tc_fence_after();
@@ -713,7 +714,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS3, 1)
 #pragma unroll
                         for (int kk = 0; kk < BK / 16; ++kk)
                             umma_f16_2sm_ts(tmem_base, a0 + kk * 8, umma_desc_sw128(b0 + kk * 32), kIdesc,
-                                            (ks | kk) != 0);
+                                            (ks != p.c_lo * p.spc) || (kk != 0));
                         umma_commit_2sm(&wempty[ws], 0x3);
                         umma_commit_2sm(&xempty[xs], 0x3);
                     }
@@ -776,7 +777,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS3, 1)
             const int f = n * 256 + (int)rank * 128 + row;
             const bool valid = f < p.F;
 #pragma unroll 1
-            for (int c = 0; c < p.n_chunks; ++c) {
+            for (int c = p.c_lo; c < p.c_hi; ++c) {
                 uint32_t e[Mi][BPC];
                 const uint8_t* src = p.P16 + ((int64_t)c * Mi * p.F_pad + f) * kUB;
 #pragma unroll
@@ -901,7 +902,7 @@ static cudaError_t launch_one(const CUtensorMap& A, const CUtensorMap& B, const 
 int ksplit_for(const Plan& p, int tiles) {
     int best = 1;
     double best_t = 1e30;
-    for (int S = 1; S <= MAX_KSPLIT && S <= p.L.n_chunks; ++S) {
+    for (int S = 1; S <= MAX_KSPLIT && S <= p.c_hi - p.c_lo; ++S) {
         const double waves = (double)((tiles * S + p.num_sms - 1) / p.num_sms);
         const double t = waves / S;
         if (t < best_t - 1e-9) {
@@ -912,8 +913,20 @@ int ksplit_for(const Plan& p, int tiles) {
     return best;
 }
 
+void set_band(Plan& p, int k_lo, int k_hi, const uint8_t* mask, int64_t mask_stride) {
+    p.k_lo = k_lo;
+    p.k_hi = k_hi;
+    p.c_lo = k_lo / p.L.bpc;
+    p.c_hi = (k_hi + p.L.bpc - 1) / p.L.bpc;
+    p.mask = mask;
+    p.mask_stride = mask_stride;
+}
+
 cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
     GemmParams gp{};
+    const bool producer_mode = (mode == 0 || mode == 1 || mode == 3);
+    gp.c_lo = producer_mode ? p.c_lo : 0;
+    gp.c_hi = producer_mode ? p.c_hi : 0;
     gp.P16 = p.d_P16;
     gp.F = F;
     gp.F_pad = (int)p.F_pad;

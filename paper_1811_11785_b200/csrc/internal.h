@@ -86,6 +86,10 @@ struct Plan {
     float* d_score_stage = nullptr;
     int64_t last_frames = 0;
     int last_method = 0;
+    // per-call band limit (NEXT-3): bins [k_lo, k_hi) -> active chunks [c_lo, c_hi); optional per-frame TF mask
+    int k_lo = 0, k_hi = 0, c_lo = 0, c_hi = 0;
+    const uint8_t* mask = nullptr;
+    int64_t mask_stride = 0;
     // per-stage profiling
     bool prof_on = false;
     int prof_cap = 0, prof_n = 0;
@@ -114,6 +118,7 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s);
 cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s);
 constexpr int MAX_KSPLIT = 4;
 int ksplit_for(const Plan& p, int tiles);   // K splits of the SVD projection GEMM for its tile count
+void set_band(Plan& p, int k_lo, int k_hi, const uint8_t* mask, int64_t mask_stride);
 // method SRP|SVD|BOTH; doa[0]/score[0] receive SRP results, doa[1]/score[1] SVD results
 cudaError_t launch_finalize(const Plan& p, int method, int F, int32_t* const doa[2], float* const score[2],
                             cudaStream_t s);

@@ -61,7 +61,7 @@ template <int R, int BPC>
 __global__ void __launch_bounds__(32 * STFT_WARPS)
     stft_phat_kernel(const float* __restrict__ audio, int64_t cs, int64_t fstride, int F, int Mi, int64_t F_pad,
                      const float* __restrict__ win, const float2* __restrict__ twN, uint8_t* __restrict__ P16,
-                     int n_chunks) {
+                     int n_chunks, int k_lo, int k_hi, const uint8_t* __restrict__ mask, int64_t mask_stride) {
     constexpr int bpc = BPC;
     constexpr int N = 64 * R;
     constexpr int H = N / 2;
@@ -137,7 +137,8 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
     // ---- real-FFT post pass + PHAT per bin (lanes over consecutive bins), halves into the padded record tile
     for (int k = lane; k < n_chunks * bpc; k += 32) {
         float2 e = make_float2(0.f, 0.f);
-        if (live && k < Kb) {
+        // bins outside the band [k_lo, k_hi) or masked out for this frame contribute nothing (NEXT-3)
+        if (live && k < Kb && k >= k_lo && k < k_hi && (!mask || mask[(int64_t)f * mask_stride + k])) {
             const int k0 = k & (H - 1), km = (H - k) & (H - 1);
             const float2 Zk = wbuf[k0 + (k0 >> 5)];
             const float2 Zm = wbuf[km + (km >> 5)];
@@ -169,7 +170,8 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
 __global__ void stft_phat_small_kernel(const float* __restrict__ audio, int64_t cs, int64_t fstride, int F, int Mi,
                                        int64_t F_pad, int N, const float* __restrict__ win,
                                        const float2* __restrict__ twN, uint8_t* __restrict__ P16, int bpc,
-                                       int n_chunks) {
+                                       int n_chunks, int k_lo, int k_hi, const uint8_t* __restrict__ mask,
+                                       int64_t mask_stride) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m = blockIdx.y;
     const int f = blockIdx.x * STFT_WARPS + warp;
@@ -177,7 +179,8 @@ __global__ void stft_phat_small_kernel(const float* __restrict__ audio, int64_t 
     const int Kb = N / 2 + 1;
     const float* x = audio + (int64_t)m * cs + (int64_t)f * fstride;
     __shared__ float2 e_s[STFT_WARPS][32];
-    if (lane < Kb) {
+    e_s[warp][lane] = make_float2(0.f, 0.f);
+    if (lane < Kb && lane >= k_lo && lane < k_hi && (!mask || mask[(int64_t)f * mask_stride + lane])) {
         float2 X = make_float2(0.f, 0.f);
         for (int n = 0; n < N; ++n) {
             const float2 w = __ldg(twN + ((lane * n) % N));
@@ -224,7 +227,8 @@ static cudaError_t launch_rb(const Plan& p, const float* audio, int64_t cs, int6
     }
     dim3 grid((F + STFT_WARPS - 1) / STFT_WARPS, p.M);
     stft_phat_kernel<R, BPC><<<grid, 32 * STFT_WARPS, smem, s>>>(audio, cs, fstride, F, p.L.Mi, p.F_pad, p.d_window,
-                                                                 p.d_twN, p.d_P16, p.L.n_chunks);
+                                                                 p.d_twN, p.d_P16, p.L.n_chunks, p.k_lo, p.k_hi,
+                                                                 p.mask, p.mask_stride);
     return cudaGetLastError();
 }
 
@@ -247,7 +251,8 @@ cudaError_t launch_stft_phat(const Plan& p, const float* audio, int64_t cs, int6
     }
     dim3 grid((F + STFT_WARPS - 1) / STFT_WARPS, p.M);
     stft_phat_small_kernel<<<grid, 32 * STFT_WARPS, 0, s>>>(audio, cs, fstride, F, p.L.Mi, p.F_pad, p.N, p.d_window,
-                                                           p.d_twN, p.d_P16, p.L.bpc, p.L.n_chunks);
+                                                           p.d_twN, p.d_P16, p.L.bpc, p.L.n_chunks, p.k_lo, p.k_hi,
+                                                           p.mask, p.mask_stride);
     return cudaGetLastError();
 }
 

@@ -428,3 +428,63 @@ def test_topk_two_sources_small(method):
     rate = _topk_compare(q, P_ref, grid, srp.steering_classes(tau), k, sep, f"topk {method}")
     assert rate >= 0.9, rate
     plan.close()
+
+
+@pytest.mark.parametrize("cfg,frames", [(2, 300), (5, 256)])
+def test_tf_mask_and_band(cfg, frames):
+    """NEXT-3: band limit [k_lo, k_hi) + per-frame binary mask, both methods, against the oracle's X with
+    the excluded entries set to 0."""
+    w = make(cfg, frames)
+    F, K = w.n_frames, w.N // 2 + 1
+    plan = _plan(w, max_frames=F)
+    tau = srp.tdoa(w.mics, w.points, w.fs, w.c, w.field)
+    fac = svd.svd_factors(tau, w.N, w.delta)
+    rng = np.random.default_rng(cfg + 7)
+    k_lo, k_hi = 13, 203
+    keep = rng.random((F, K)) < 0.7
+    keep[:, :k_lo] = False
+    keep[:, k_hi:] = False
+    keep[3] = False                                                # one frame fully masked: degenerate
+    audio = torch.from_numpy(w.audio).to(DEV)
+    mask = torch.from_numpy(keep.astype(np.uint8)).to(DEV)
+    x = srp.apply_tf_mask(srp.frames_to_x(PP._frames_subset(w, np.arange(F))), w.M * (w.M - 1) // 2, keep)
+    for method in ("srp", "svd"):
+        d = torch.empty(F, dtype=torch.int32, device=DEV)
+        sc = torch.empty(F, dtype=torch.float32, device=DEV)
+        plan.localize_masked(method, audio, F, w.channel_stride, w.frame_stride, k_lo, k_hi, mask, K, d, sc,
+                             torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        q, s = d.cpu().numpy(), sc.cpu().numpy()
+        assert q[3] == -1 and s[3] == 0.0
+        keepf = _check_degenerate(q, s, x)
+        P_, Y_at = (PP.srp_reference(tau, x[keepf], w.N) if method == "srp"
+                    else PP.svd_reference(fac, tau, x[keepf], w.N))
+        print(cfg, method, PP.compare(q[keepf], s[keepf], P_, Y_at, f"cfg{cfg} masked {method}"))
+    plan.close()
+
+
+def test_band_limit_reduces_work():
+    """The band limit is skipped by the GEMMs: half the bins -> well under the full-band time (cfg3 batch)."""
+    w = make(3, 4096)
+    plan = _plan(w, methods=("srp",), max_frames=w.n_frames)
+    audio = torch.from_numpy(w.audio).to(DEV)
+    F, K = w.n_frames, w.N // 2 + 1
+    d = torch.empty(F, dtype=torch.int32, device=DEV)
+    sc = torch.empty(F, dtype=torch.float32, device=DEV)
+    st = torch.cuda.current_stream().cuda_stream
+
+    def run(k_hi):
+        for _ in range(2):
+            plan.localize_masked("srp", audio, F, w.channel_stride, w.frame_stride, 0, k_hi, None, 0, d, sc, st)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(3):
+            plan.localize_masked("srp", audio, F, w.channel_stride, w.frame_stride, 0, k_hi, None, 0, d, sc, st)
+        e1.record()
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1) / 3
+    full, half = run(K), run(K // 2)
+    print("band full %.2f ms, half %.2f ms" % (full, half))
+    assert half < 0.7 * full
+    plan.close()
