@@ -34,7 +34,7 @@ def _args():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cfg", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-frames", type=int, default=8)
+    ap.add_argument("--cpu-frames", type=int, default=32)
     return ap.parse_args()
 
 
@@ -152,7 +152,7 @@ def run_reference(a) -> None:
         return
     from workloads import make
     w = make(a.cfg)
-    per = 1  # frames per step: one oracle pass regenerates the whole W (~20 s at cfg3)
+    per = 2  # frames per step: one oracle pass regenerates the whole W (~20-35 s at cfg3)
     for _ in range(a.warmup):
         cpu_baseline(w, per)
     t = []
@@ -166,7 +166,7 @@ def run_reference(a) -> None:
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"cfg{a.cfg}", "frames_per_step": per},
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
-                             "sample": f"{per} cfg{a.cfg} frame per step through the oracle's SRP-PHAT path"},
+                             "sample": f"{per} cfg{a.cfg} frames per step through the oracle SRP-PHAT path (W regenerated per step)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
