@@ -116,6 +116,18 @@ svdphat_status svdphat_localize_host(svdphat_plan_t plan, int32_t method, const 
                                      int64_t audio_elems, int64_t n_frames, int64_t channel_stride,
                                      int64_t frame_stride, int32_t* h_doa, float* h_score, void* stream);
 
+/* Streaming host path: enqueue one batch (H2D copy of audio elements [0, audio_elems) on an internal upload
+ * stream, localisation on `stream`, D2H of the results on an internal download stream) and return at once with a
+ * ticket.  Two batches may be in flight per plan (double-buffered device staging, allocated on first use): the
+ * upload of batch i+1 overlaps the kernels of batch i.  A third submit first waits for the oldest batch.  Host
+ * buffers must stay valid and unmodified until svdphat_wait(ticket) returns (pinned memory for full bandwidth).
+ * Outputs as svdphat_localize_host. */
+svdphat_status svdphat_submit_host(svdphat_plan_t plan, int32_t method, const float* h_audio, int64_t audio_elems,
+                                   int64_t n_frames, int64_t channel_stride, int64_t frame_stride, int32_t* h_doa,
+                                   float* h_score, void* stream, int64_t* ticket);
+/* Blocks until the batch of `ticket` has been copied back (INVALID_ARG for an unknown ticket). */
+svdphat_status svdphat_wait(svdphat_plan_t plan, int64_t ticket);
+
 /* Multi-source extension (future work: "investigate multiple source localization").  For each frame,
  * the k (1..4) strongest peaks of the method's power map — SRP: Y_q (eq. 5); SVD: Re{D_hat_q . Z_hat} (eq. 14) —
  * taken greedily, each peak excluding all candidates whose direction is within min_sep_deg of a stronger peak

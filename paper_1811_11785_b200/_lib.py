@@ -55,6 +55,8 @@ def _load() -> C.CDLL:
         "svdphat_profile_begin": (st, [vp, i32]),
         "svdphat_localize_topk": (st, [vp, i32, vp, i64, i64, i64, i32, C.c_double, vp, vp, vp]),
         "svdphat_localize_masked": (st, [vp, i32, vp, i64, i64, i64, i32, i32, vp, i64, vp, vp, vp]),
+        "svdphat_submit_host": (st, [vp, i32, vp, i64, i64, i64, i64, vp, vp, vp, C.POINTER(i64)]),
+        "svdphat_wait": (st, [vp, i64]),
         "svdphat_profile_end": (i32, [vp, C.POINTER(i32), C.POINTER(C.c_float), i32]),
     }
     for name, (res, args) in sig.items():
@@ -142,6 +144,18 @@ class Plan:
         _check(lib.svdphat_localize_topk(self._h, _METHOD[method], _ptr(audio), n_frames, channel_stride,
                                          frame_stride, k, min_sep_deg, _ptr(doa), _ptr(score), stream),
                "svdphat_localize_topk")
+
+    def submit_host(self, method: str, audio, audio_elems: int, n_frames: int, channel_stride: int,
+                    frame_stride: int, doa, score, stream: int = 0) -> int:
+        """Streaming host path: enqueue H2D -> localise -> D2H and return a ticket (two batches in flight)."""
+        t = C.c_int64()
+        _check(lib.svdphat_submit_host(self._h, _METHOD[method], _ptr(audio), audio_elems, n_frames, channel_stride,
+                                       frame_stride, _ptr(doa), _ptr(score), stream, C.byref(t)),
+               "svdphat_submit_host")
+        return t.value
+
+    def wait(self, ticket: int) -> None:
+        _check(lib.svdphat_wait(self._h, ticket), "svdphat_wait")
 
     def localize_masked(self, method: str, audio, n_frames: int, channel_stride: int, frame_stride: int, k_lo: int,
                         k_hi: int, mask, mask_stride: int, doa, score, stream: int = 0) -> None:

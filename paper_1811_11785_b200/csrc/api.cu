@@ -128,6 +128,16 @@ struct svdphat_plan_s {
             if (p.ev_done[i]) cudaEventDestroy(p.ev_done[i]);
         }
         if (p.copy_stream) cudaStreamDestroy(p.copy_stream);
+        for (auto& sl : p.slots) {
+            if (sl.d_audio) cudaFree(sl.d_audio);
+            if (sl.d_doa) cudaFree(sl.d_doa);
+            if (sl.d_score) cudaFree(sl.d_score);
+            if (sl.h2d) cudaEventDestroy(sl.h2d);
+            if (sl.comp) cudaEventDestroy(sl.comp);
+            if (sl.d2h) cudaEventDestroy(sl.d2h);
+        }
+        if (p.up_stream) cudaStreamDestroy(p.up_stream);
+        if (p.down_stream) cudaStreamDestroy(p.down_stream);
         if (p.ev_fork) cudaEventDestroy(p.ev_fork);
         if (p.ev_join) cudaEventDestroy(p.ev_join);
         if (p.svd_stream) cudaStreamDestroy(p.svd_stream);
@@ -628,6 +638,73 @@ svdphat_status svdphat_localize_host(svdphat_plan_t plan, int32_t method, const 
     SVD_CUDA_TRY(cudaMemcpyAsync(h_score, p.d_score_stage, nout * sizeof(float), cudaMemcpyDeviceToHost, s));
     SVD_CUDA_TRY(cudaStreamSynchronize(s));
     p.last_frames = F;
+    return SVDPHAT_OK;
+}
+
+svdphat_status svdphat_submit_host(svdphat_plan_t plan, int32_t method, const float* h_audio, int64_t audio_elems,
+                                   int64_t n_frames, int64_t channel_stride, int64_t frame_stride, int32_t* h_doa,
+                                   float* h_score, void* stream, int64_t* ticket) {
+    if (!plan || !ticket) return fail(SVDPHAT_INVALID_ARG, "NULL argument");
+    Plan& p = plan->p;
+    svdphat_status st = check_localize_args(p, method, n_frames, channel_stride, frame_stride);
+    if (st != SVDPHAT_OK) return st;
+    if (n_frames == 0) return fail(SVDPHAT_INVALID_ARG, "n_frames must be > 0");
+    if (!h_audio || !h_doa || !h_score || audio_elems <= 0) return fail(SVDPHAT_INVALID_ARG, "NULL/empty buffer");
+    const int64_t need = (int64_t)(p.M - 1) * channel_stride + (n_frames - 1) * frame_stride + p.N;
+    if (need > audio_elems) return fail(SVDPHAT_INVALID_ARG, "audio buffer smaller than the addressed frames");
+    SVD_CUDA_TRY(cudaSetDevice(p.device));
+    if (!p.up_stream) {
+        SVD_CUDA_TRY(cudaStreamCreateWithFlags(&p.up_stream, cudaStreamNonBlocking));
+        SVD_CUDA_TRY(cudaStreamCreateWithFlags(&p.down_stream, cudaStreamNonBlocking));
+        for (auto& sl : p.slots) {
+            SVD_CUDA_TRY(cudaEventCreateWithFlags(&sl.h2d, cudaEventDisableTiming));
+            SVD_CUDA_TRY(cudaEventCreateWithFlags(&sl.comp, cudaEventDisableTiming));
+            SVD_CUDA_TRY(cudaEventCreateWithFlags(&sl.d2h, cudaEventDisableTiming));
+        }
+    }
+    Plan::HostSlot& sl = p.slots[p.next_ticket & 1];
+    if (sl.ticket >= 0) SVD_CUDA_TRY(cudaEventSynchronize(sl.d2h));     // the slot's previous batch is done
+    if (need > sl.elems) {
+        if (sl.d_audio) cudaFree(sl.d_audio);
+        sl.d_audio = nullptr;
+        sl.elems = 0;
+        if (cudaMalloc(&sl.d_audio, need * sizeof(float)) != cudaSuccess)
+            return fail(SVDPHAT_ALLOC, "streaming staging allocation failed");
+        sl.elems = need;
+    }
+    if (!sl.d_doa) {
+        if (cudaMalloc(&sl.d_doa, 2 * p.F_pad * sizeof(int32_t)) != cudaSuccess ||
+            cudaMalloc(&sl.d_score, 2 * p.F_pad * sizeof(float)) != cudaSuccess)
+            return fail(SVDPHAT_ALLOC, "streaming result allocation failed");
+    }
+    cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+    const int F = (int)n_frames;
+    const bool both = method == SVDPHAT_METHOD_BOTH;
+    SVD_CUDA_TRY(cudaMemcpyAsync(sl.d_audio, h_audio, need * sizeof(float), cudaMemcpyHostToDevice, p.up_stream));
+    SVD_CUDA_TRY(cudaEventRecord(sl.h2d, p.up_stream));
+    SVD_CUDA_TRY(cudaStreamWaitEvent(s, sl.h2d, 0));
+    st = localize_impl(p, method, sl.d_audio, F, channel_stride, frame_stride, sl.d_doa, sl.d_score,
+                       sl.d_doa + (both ? F : 0), sl.d_score + (both ? F : 0), s);
+    if (st != SVDPHAT_OK) return st;
+    SVD_CUDA_TRY(cudaEventRecord(sl.comp, s));
+    SVD_CUDA_TRY(cudaStreamWaitEvent(p.down_stream, sl.comp, 0));
+    const int64_t nout = (both ? 2 : 1) * (int64_t)F;
+    SVD_CUDA_TRY(cudaMemcpyAsync(h_doa, sl.d_doa, nout * sizeof(int32_t), cudaMemcpyDeviceToHost, p.down_stream));
+    SVD_CUDA_TRY(cudaMemcpyAsync(h_score, sl.d_score, nout * sizeof(float), cudaMemcpyDeviceToHost, p.down_stream));
+    SVD_CUDA_TRY(cudaEventRecord(sl.d2h, p.down_stream));
+    sl.ticket = p.next_ticket;
+    *ticket = p.next_ticket++;
+    return SVDPHAT_OK;
+}
+
+svdphat_status svdphat_wait(svdphat_plan_t plan, int64_t ticket) {
+    if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
+    Plan& p = plan->p;
+    if (ticket < 0 || ticket >= p.next_ticket) return fail(SVDPHAT_INVALID_ARG, "unknown ticket");
+    const Plan::HostSlot& sl = p.slots[ticket & 1];
+    if (sl.ticket != ticket) return SVDPHAT_OK;                          // slot reused: that batch completed
+    SVD_CUDA_TRY(cudaSetDevice(p.device));
+    SVD_CUDA_TRY(cudaEventSynchronize(sl.d2h));
     return SVDPHAT_OK;
 }
 

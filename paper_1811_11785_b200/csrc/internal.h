@@ -86,6 +86,17 @@ struct Plan {
     float* d_score_stage = nullptr;
     int64_t last_frames = 0;
     int last_method = 0;
+    // streaming host path (svdphat_submit_host): two staging slots
+    struct HostSlot {
+        float* d_audio = nullptr;
+        int64_t elems = 0;
+        int32_t* d_doa = nullptr;
+        float* d_score = nullptr;
+        cudaEvent_t h2d = nullptr, comp = nullptr, d2h = nullptr;
+        int64_t ticket = -1;
+    } slots[2];
+    cudaStream_t up_stream = nullptr, down_stream = nullptr;
+    int64_t next_ticket = 0;
     // per-call band limit (NEXT-3): bins [k_lo, k_hi) -> active chunks [c_lo, c_hi); optional per-frame TF mask
     int k_lo = 0, k_hi = 0, c_lo = 0, c_hi = 0;
     const uint8_t* mask = nullptr;

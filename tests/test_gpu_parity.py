@@ -488,3 +488,26 @@ def test_band_limit_reduces_work():
     print("band full %.2f ms, half %.2f ms" % (full, half))
     assert half < 0.7 * full
     plan.close()
+
+
+def test_streaming_submit_matches_device_path():
+    """svdphat_submit_host: three batches in flight/queued, each equal to the device-path result."""
+    w = make(3, 3000)
+    plan = _plan(w, max_frames=w.n_frames)
+    F = w.n_frames
+    audio = torch.from_numpy(w.audio).to(DEV)
+    d = torch.empty(2 * F, dtype=torch.int32, device=DEV)
+    sc = torch.empty(2 * F, dtype=torch.float32, device=DEV)
+    st = torch.cuda.current_stream().cuda_stream
+    plan.localize("both", audio, F, w.channel_stride, w.frame_stride, d, sc, st)
+    torch.cuda.synchronize()
+    ref_d, ref_s = d.cpu().numpy(), sc.cpu().numpy()
+    h_audio = torch.from_numpy(w.audio).pin_memory()
+    outs = [(torch.empty(2 * F, dtype=torch.int32).pin_memory(), torch.empty(2 * F).pin_memory()) for _ in range(3)]
+    tickets = [plan.submit_host("both", h_audio, w.audio.size, F, w.channel_stride, w.frame_stride, o[0], o[1], st)
+               for o in outs]
+    for t in tickets:
+        plan.wait(t)
+    for od, os_ in outs:
+        assert np.array_equal(od.numpy(), ref_d) and np.array_equal(os_.numpy(), ref_s)
+    plan.close()
