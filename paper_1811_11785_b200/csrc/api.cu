@@ -145,7 +145,7 @@ struct svdphat_plan_s {
         if (p.ev_join2) cudaEventDestroy(p.ev_join2);
         void* bufs[] = {p.d_W16,   p.d_V16,   p.d_R16,   p.d_rep,   p.d_delay,     p.d_window,      p.d_twN,
                         p.d_P16,   p.d_keys,  p.d_Z32,   p.d_Zs16,  p.d_zflag,     p.d_stage,       p.d_doa_stage,
-                        p.d_score_stage, p.d_S, p.d_cls, p.d_dirs};
+                        p.d_score_stage, p.d_S, p.d_cls, p.d_dirs, p.d_Ypart};
         for (void* b : bufs)
             if (b) cudaFree(b);
     }
@@ -361,15 +361,32 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     SVD_CUDA_TRY(cudaMalloc(&p.d_keys, 2 * Fp * sizeof(unsigned long long)));
     p.bytes_ws = bytes_P16 + 2 * Fp * 8;
     if (p.methods & SVDPHAT_METHOD_SVD) {
-        SVD_CUDA_TRY(cudaMalloc(&p.d_Z32, MAX_KSPLIT * Fp * 2 * p.Dh * sizeof(float)));
-        SVD_CUDA_TRY(cudaMemset(p.d_Z32, 0, MAX_KSPLIT * Fp * 2 * p.Dh * sizeof(float)));
+        // split-K partial buffers: as many splits (<= MAX_KSPLIT) as fit in ~256 MB
+        const int64_t zbytes = Fp * 2 * p.Dh * (int64_t)sizeof(float);
+        p.zsplit_max = (int)std::max<int64_t>(1, std::min<int64_t>(MAX_KSPLIT, (256ll << 20) / zbytes));
+        SVD_CUDA_TRY(cudaMalloc(&p.d_Z32, p.zsplit_max * zbytes));
+        SVD_CUDA_TRY(cudaMemset(p.d_Z32, 0, p.zsplit_max * zbytes));
         SVD_CUDA_TRY(cudaMalloc(&p.d_Zs16, Fp * p.K2 * 2));
         SVD_CUDA_TRY(cudaMemset(p.d_Zs16, 0, Fp * p.K2 * 2));
         SVD_CUDA_TRY(cudaMalloc(&p.d_zflag, Fp * sizeof(int)));
         SVD_CUDA_TRY(cudaMemset(p.d_zflag, 0, Fp * sizeof(int)));
-        p.bytes_ws += MAX_KSPLIT * Fp * 2 * p.Dh * 4 + Fp * p.K2 * 2 + Fp * 4;
+        p.bytes_ws += p.zsplit_max * Fp * 2 * p.Dh * 4 + Fp * p.K2 * 2 + Fp * 4;
         if (!encode_2d(&p.tm_Zs, p.d_Zs16, Fp, p.K2, 256))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(Zs) failed");
+    }
+    // small batches (fewer SRP tile units than half the CTA pairs): split-K partial power maps, <= 64 MB
+    if ((p.methods & SVDPHAT_METHOD_SRP) && p.pair_srp) {
+        const int64_t units = (int64_t)(p.Q_pad / 256) * ((p.max_frames + 255) / 256);
+        if (units * 2 <= p.num_sms / 2) {
+            const int64_t ybytes = Fp * (int64_t)p.Q_pad * (int64_t)sizeof(float);
+            p.srp_split_max = (int)std::min<int64_t>(8, std::max<int64_t>(1, (64ll << 20) / ybytes));
+            if (p.srp_split_max > 1) {
+                SVD_CUDA_TRY(cudaMalloc(&p.d_Ypart, p.srp_split_max * ybytes));
+                p.bytes_ws += p.srp_split_max * ybytes;
+            } else {
+                p.srp_split_max = 0;
+            }
+        }
     }
     SVD_CUDA_TRY(gemm_set_attributes());
     if ((p.methods & SVDPHAT_METHOD_BOTH) == SVDPHAT_METHOD_BOTH) {

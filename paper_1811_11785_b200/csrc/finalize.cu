@@ -13,6 +13,11 @@
 
 namespace svdphat {
 
+__device__ __forceinline__ uint32_t f2o_dev(float v) {   // order-preserving float -> uint32 (as ptx.cuh f2o)
+    const uint32_t b = __float_as_uint(v);
+    return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
+}
+
 // Z = sum of the nsplit partial projections (fixed order: deterministic), then normalise and split.
 __global__ void zsplit_kernel(float* __restrict__ Z, int F, int64_t F_pad, int ldz, int nsplit,
                               __half* __restrict__ Zs, int K2, int* __restrict__ zflag) {
@@ -167,6 +172,34 @@ __global__ void __launch_bounds__(32 * FIN_WARPS)
             o.score[j][(int64_t)f * o.out_stride] = dead ? 0.f : 0.5f * y;
         }
     }
+}
+
+// Small-batch SRP: Y[f][q] = sum of the S partial power maps (fixed order: deterministic), argmax over the steering
+// classes (lowest index on ties) -> the frame's key.  Warp per frame.
+__global__ void split_argmax_kernel(const float* __restrict__ Yp, int S, int64_t F_pad, int ldq, int Q, int F,
+                                    unsigned long long* __restrict__ keys) {
+    const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (f >= F) return;
+    unsigned long long best = 0ull;
+    for (int q = lane; q < Q; q += 32) {
+        float v = 0.f;
+        for (int s = 0; s < S; ++s) v += Yp[((int64_t)s * F_pad + f) * ldq + q];
+        const unsigned long long k = v == v ? ((unsigned long long)f2o_dev(v) << 32) | (0xFFFFFFFFull - (uint32_t)q) : 0ull;
+        best = k > best ? k : best;
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+        const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
+        best = ob > best ? ob : best;
+    }
+    if (lane == 0) keys[f] = best;
+}
+
+cudaError_t launch_split_argmax(const Plan& p, int F, int S, cudaStream_t s) {
+    if (F <= 0) return cudaSuccess;
+    split_argmax_kernel<<<(F * 32 + 255) / 256, 256, 0, s>>>(p.d_Ypart, S, p.F_pad, p.Q_pad, p.Q_eff, F, p.d_keys);
+    return cudaGetLastError();
 }
 
 cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s) {

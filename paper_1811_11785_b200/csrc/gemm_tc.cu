@@ -900,11 +900,14 @@ static cudaError_t launch_one(const CUtensorMap& A, const CUtensorMap& B, const 
 }
 
 int ksplit_for(const Plan& p, int tiles) {
+    // time ~ waves x (slabs per unit + fixed per-unit cost of filling/draining the pipeline and the epilogue)
+    const int nc = p.c_hi - p.c_lo;
+    const double slabs = (double)nc * (p.L.U / 8);
     int best = 1;
-    double best_t = 1e30;
-    for (int S = 1; S <= MAX_KSPLIT && S <= p.c_hi - p.c_lo; ++S) {
+    double best_t = 1e300;
+    for (int S = 1; S <= p.zsplit_max && S <= nc; ++S) {
         const double waves = (double)((tiles * S + p.num_sms - 1) / p.num_sms);
-        const double t = waves / S;
+        const double t = waves * (slabs / S + 24.0);
         if (t < best_t - 1e-9) {
             best_t = t;
             best = S;
@@ -1033,6 +1036,32 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
         SVD_DISPATCH3(32, 2)
 #undef SVD_DISPATCH3
         return cudaErrorInvalidValue;
+    }
+    if (mode == 0 && p.pair_srp && p.srp_split_max > 1) {
+        // small batch: fewer units than half the CTA pairs -> split K into chunk ranges with partial power maps
+        const int m2 = p.Q_pad / 256, units = m2 * gp.n_tiles, npairs = p.num_sms / 2;
+        int S = units > 0 ? npairs / units : 1;
+        S = S < p.srp_split_max ? S : p.srp_split_max;
+        S = S < p.c_hi - p.c_lo ? S : p.c_hi - p.c_lo;
+        if (units * 2 <= npairs && S > 1) {
+            gp.m_tiles = m2;
+            gp.ksplit = S;
+            gp.Z = p.d_Ypart;
+            gp.ldz = p.Q_pad;
+            const int pairs = units * S < npairs ? units * S : npairs;
+#define SVD_DISPATCH5(MI, BP)                                                                 \
+    if (p.L.Mi == MI) {                                                                      \
+        gemm2_kernel<MI, BP, 1><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(*A, *B, gp);         \
+        cudaError_t e = cudaGetLastError();                                                  \
+        return e != cudaSuccess ? e : launch_split_argmax(p, F, S, s);                       \
+    }
+            SVD_DISPATCH5(4, 4)
+            SVD_DISPATCH5(8, 4)
+            SVD_DISPATCH5(16, 4)
+            SVD_DISPATCH5(32, 2)
+#undef SVD_DISPATCH5
+            return cudaErrorInvalidValue;
+        }
     }
     if (mode == 0 && p.pair_srp) {
         gp.m_tiles = p.Q_pad / 256;

@@ -56,7 +56,11 @@ struct Plan {
     // workspace
     uint8_t* d_P16 = nullptr;     // phasors
     unsigned long long* d_keys = nullptr;  // [2][F_pad]: SRP keys, SVD search keys
-    float* d_Z32 = nullptr;       // [MAX_KSPLIT][F_pad][2*Dh] partial Z of the split-K projection
+    float* d_Z32 = nullptr;       // [zsplit_max][F_pad][2*Dh] partial Z of the split-K projection
+    int zsplit_max = 1;
+    // small batches: SRP as split-K partial power maps + sum/argmax (the argmax epilogue cannot split K)
+    float* d_Ypart = nullptr;     // [srp_split_max][F_pad][Q_pad]
+    int srp_split_max = 0;
     __half* d_Zs16 = nullptr;     // [F_pad][K2]
     int* d_zflag = nullptr;       // [F_pad]
     // multi-source (top-k) workspace, allocated on first use: power map S[F_pad][Q_pad], class lists [F_pad][4]
@@ -127,7 +131,8 @@ cudaError_t launch_stft_phat(const Plan& p, const float* audio, int64_t cs, int6
 //       2 = SVD search argmax (A = R16, B = Zs16 via TMA), 3 = SRP power map -> d_S, 4 = SVD search power map -> d_S
 cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s);
 cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s);
-constexpr int MAX_KSPLIT = 4;
+cudaError_t launch_split_argmax(const Plan& p, int F, int S, cudaStream_t s);
+constexpr int MAX_KSPLIT = 32;               // cap on K splits (chunk ranges) of the store-mode GEMMs
 int ksplit_for(const Plan& p, int tiles);   // K splits of the SVD projection GEMM for its tile count
 void set_band(Plan& p, int k_lo, int k_hi, const uint8_t* mask, int64_t mask_stride);
 // method SRP|SVD|BOTH; doa[0]/score[0] receive SRP results, doa[1]/score[1] SVD results
