@@ -283,6 +283,10 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
         p.pair_srp = e ? atoi(e) != 0 : true;
     }
     p.Q_pad = p.pair_srp ? (p.Q_eff + 255) / 256 * 256 : (p.Q_eff + 127) / 128 * 128;
+    {
+        const char* e = getenv("SVDPHAT_PAIR_PROJ");
+        p.pair_proj = e ? atoi(e) != 0 : true;
+    }
 
     // ---- device tables
     std::vector<double> tau_cls((size_t)p.Q_eff * P);
@@ -347,7 +351,7 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     if (p.methods & SVDPHAT_METHOD_SVD) {
         st = setup_svd_operands(p, d_tau, d->rank_D);
         if (st != SVDPHAT_OK) return st;
-        if (!encode_2d(&p.tm_V, p.d_V16, 2 * p.Dh, p.L.K_total, 128))
+        if (!encode_2d(&p.tm_V, p.d_V16, p.V_rows, p.L.K_total, 128))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(V) failed");
         if (!encode_2d(&p.tm_R, p.d_R16, p.Q_pad, p.K2, 128))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(R) failed");

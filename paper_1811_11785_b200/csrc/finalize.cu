@@ -13,6 +13,12 @@
 
 namespace svdphat {
 
+// sin/cos(pi t): reduce t to [-1, 1] (one period), then the fast hardware sin/cos (|error| < 5e-7 there)
+__device__ __forceinline__ void sincospi_fast(float t, float* s, float* c) {
+    const float y = t - 2.0f * rintf(0.5f * t);
+    __sincosf(3.14159265358979f * y, s, c);
+}
+
 __device__ __forceinline__ uint32_t f2o_dev(float v) {   // order-preserving float -> uint32 (as ptx.cuh f2o)
     const uint32_t b = __float_as_uint(v);
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
@@ -130,8 +136,8 @@ __global__ void __launch_bounds__(32 * FIN_WARPS)
                     // e^{+j 2 pi k delta_m / N} for k = kb0 .. kb0+bpc-1: base rotation, then unit steps
                     const float dl = __ldg(dq[j] + m);
                     float bs, bc, ss, sc;
-                    sincospif((float)kb0 * dl * inv2N, &bs, &bc);
-                    sincospif(dl * inv2N, &ss, &sc);
+                    sincospi_fast((float)kb0 * dl * inv2N, &bs, &bc);
+                    sincospi_fast(dl * inv2N, &ss, &sc);
 #pragma unroll
                     for (int t = 0; t < 4; ++t) {
                         if (t < bpc) {
@@ -206,8 +212,7 @@ cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s) {
     if (F <= 0) return cudaSuccess;
     const int threads = 256;
     const int blocks = (F * 32 + threads - 1) / threads;
-    const int tiles = (2 * p.Dh / 128) * ((F + 255) / 256);     // same split choice as the projection GEMM
-    zsplit_kernel<<<blocks, threads, 0, s>>>(p.d_Z32, F, p.F_pad, 2 * p.Dh, ksplit_for(p, tiles), p.d_Zs16, p.K2,
+    zsplit_kernel<<<blocks, threads, 0, s>>>(p.d_Z32, F, p.F_pad, 2 * p.Dh, proj_shape(p, F).ksplit, p.d_Zs16, p.K2,
                                              p.d_zflag);
     return cudaGetLastError();
 }

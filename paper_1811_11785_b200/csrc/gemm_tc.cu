@@ -899,21 +899,27 @@ static cudaError_t launch_one(const CUtensorMap& A, const CUtensorMap& B, const 
     return cudaGetLastError();
 }
 
-int ksplit_for(const Plan& p, int tiles) {
-    // time ~ waves x (slabs per unit + fixed per-unit cost of filling/draining the pipeline and the epilogue)
+// SVD projection launch shape: CTA-pair tiles of 256 V rows (p.pair_proj) or 1-CTA tiles of 128, and its K splits
+ProjShape proj_shape(const Plan& p, int F) {
+    ProjShape sh;
+    sh.pair = p.pair_proj;
+    const int n_tiles = (F + BN - 1) / BN;
+    sh.m_tiles = sh.pair ? p.V_rows / 256 : (2 * p.Dh) / BM;
+    const int units = sh.m_tiles * n_tiles;
+    const int slots = sh.pair ? p.num_sms / 2 : p.num_sms;
     const int nc = p.c_hi - p.c_lo;
     const double slabs = (double)nc * (p.L.U / 8);
-    int best = 1;
     double best_t = 1e300;
+    sh.ksplit = 1;
     for (int S = 1; S <= p.zsplit_max && S <= nc; ++S) {
-        const double waves = (double)((tiles * S + p.num_sms - 1) / p.num_sms);
+        const double waves = (double)((units * S + slots - 1) / slots);
         const double t = waves * (slabs / S + 24.0);
         if (t < best_t - 1e-9) {
             best_t = t;
-            best = S;
+            sh.ksplit = S;
         }
     }
-    return best;
+    return sh;
 }
 
 void set_band(Plan& p, int k_lo, int k_hi, const uint8_t* mask, int64_t mask_stride) {
@@ -1008,8 +1014,26 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
     }
     int tiles = gp.m_tiles * gp.n_tiles;
     if (mode == 1) {
-        // split K (at chunk boundaries) to fill the SMs: minimise waves / split, deterministic partial buffers
-        gp.ksplit = ksplit_for(p, tiles);
+        // split K (at chunk boundaries) to fill the SMs, deterministic partial buffers
+        const ProjShape sh = proj_shape(p, F);
+        gp.ksplit = sh.ksplit;
+        if (sh.pair) {
+            gp.m_tiles = sh.m_tiles;
+            const int units = gp.m_tiles * gp.n_tiles * gp.ksplit;
+            const int pairs = units < p.num_sms / 2 ? units : p.num_sms / 2;
+            if (units == 0) return cudaSuccess;
+#define SVD_DISPATCH6(MI, BP)                                                                 \
+    if (p.L.Mi == MI) {                                                                      \
+        gemm2_kernel<MI, BP, 1><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(*A, *B, gp);         \
+        return cudaGetLastError();                                                           \
+    }
+            SVD_DISPATCH6(4, 4)
+            SVD_DISPATCH6(8, 4)
+            SVD_DISPATCH6(16, 4)
+            SVD_DISPATCH6(32, 2)
+#undef SVD_DISPATCH6
+            return cudaErrorInvalidValue;
+        }
         tiles *= gp.ksplit;
     }
     const int grid = tiles < p.num_sms ? tiles : p.num_sms;

@@ -57,6 +57,8 @@ struct Plan {
     uint8_t* d_P16 = nullptr;     // phasors
     unsigned long long* d_keys = nullptr;  // [2][F_pad]: SRP keys, SVD search keys
     float* d_Z32 = nullptr;       // [zsplit_max][F_pad][2*Dh] partial Z of the split-K projection
+    int V_rows = 0;               // rows of V16 (2*Dh rounded up to 256 for the CTA-pair projection)
+    bool pair_proj = true;
     int zsplit_max = 1;
     // small batches: SRP as split-K partial power maps + sum/argmax (the argmax epilogue cannot split K)
     float* d_Ypart = nullptr;     // [srp_split_max][F_pad][Q_pad]
@@ -133,7 +135,11 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s);
 cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s);
 cudaError_t launch_split_argmax(const Plan& p, int F, int S, cudaStream_t s);
 constexpr int MAX_KSPLIT = 32;               // cap on K splits (chunk ranges) of the store-mode GEMMs
-int ksplit_for(const Plan& p, int tiles);   // K splits of the SVD projection GEMM for its tile count
+struct ProjShape {
+    bool pair;
+    int m_tiles, ksplit;
+};
+ProjShape proj_shape(const Plan& p, int F);   // tiles and K splits of the SVD projection GEMM
 void set_band(Plan& p, int k_lo, int k_hi, const uint8_t* mask, int64_t mask_stride);
 // method SRP|SVD|BOTH; doa[0]/score[0] receive SRP results, doa[1]/score[1] SVD results
 cudaError_t launch_finalize(const Plan& p, int method, int F, int32_t* const doa[2], float* const score[2],

@@ -287,7 +287,8 @@ svdphat_status setup_svd_operands(Plan& p, const double* d_tau_cls, int rank_D) 
                                    (cuDoubleComplex*)B.ptr);
         SVD_CUDA_TRY(cudaGetLastError());
     }
-    p.bytes_V = (int64_t)2 * p.Dh * p.L.K_total * 2;
+    p.V_rows = p.pair_proj ? (2 * p.Dh + 255) / 256 * 256 : 2 * p.Dh;
+    p.bytes_V = (int64_t)p.V_rows * p.L.K_total * 2;
     SVD_CUDA_TRY(cudaMalloc(&p.d_V16, p.bytes_V));
     SVD_CUDA_TRY(cudaMemset(p.d_V16, 0, p.bytes_V));
     int64_t CH = std::max<int64_t>(256, std::min<int64_t>(p.PK, (int64_t)(1ll << 30) / ((int64_t)n * 16)));

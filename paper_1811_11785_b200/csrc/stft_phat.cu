@@ -29,22 +29,90 @@ __device__ __forceinline__ float2 phat(float2 X) {
     return make_float2(0.f, 0.f);
 }
 
-// In-register radix-2 DIF DFT of R points (twiddles from the N-point table); output a[i] = DFT[bitrev_R(i)].
-template <int R>
-__device__ __forceinline__ void dft_dif(float2 (&a)[R], const float2* __restrict__ twN, int N) {
-#pragma unroll
-    for (int h = R / 2; h >= 1; h >>= 1) {
-#pragma unroll
-        for (int s0 = 0; s0 < R; s0 += 2 * h) {
-#pragma unroll
-            for (int t = 0; t < h; ++t) {
-                const float2 u = a[s0 + t], v = a[s0 + t + h];
-                a[s0 + t] = make_float2(u.x + v.x, u.y + v.y);
-                const float2 d = make_float2(u.x - v.x, u.y - v.y);
-                a[s0 + t + h] = (t == 0) ? d : cmul(d, __ldg(twN + t * (N / (2 * h))));
-            }
+// e^{-j 2 pi k / 32}, k = 0..31 (float64-rounded literals): the twiddles of every in-register DFT (R <= 32)
+struct Tw32 {
+    float c, s;
+};
+constexpr Tw32 kTw32[32] = {
+    {1.0f, -0.0f},
+    {0.9807852804032304f, -0.19509032201612825f},
+    {0.9238795325112867f, -0.3826834323650898f},
+    {0.8314696123025452f, -0.5555702330196022f},
+    {0.7071067811865476f, -0.7071067811865475f},
+    {0.5555702330196023f, -0.8314696123025452f},
+    {0.38268343236508984f, -0.9238795325112867f},
+    {0.19509032201612833f, -0.9807852804032304f},
+    {6.123233995736766e-17f, -1.0f},
+    {-0.1950903220161282f, -0.9807852804032304f},
+    {-0.3826834323650897f, -0.9238795325112867f},
+    {-0.555570233019602f, -0.8314696123025455f},
+    {-0.7071067811865475f, -0.7071067811865476f},
+    {-0.8314696123025453f, -0.5555702330196022f},
+    {-0.9238795325112867f, -0.3826834323650899f},
+    {-0.9807852804032304f, -0.1950903220161286f},
+    {-1.0f, -1.2246467991473532e-16f},
+    {-0.9807852804032304f, 0.19509032201612836f},
+    {-0.9238795325112868f, 0.38268343236508967f},
+    {-0.8314696123025455f, 0.555570233019602f},
+    {-0.7071067811865477f, 0.7071067811865475f},
+    {-0.5555702330196022f, 0.8314696123025452f},
+    {-0.38268343236509034f, 0.9238795325112865f},
+    {-0.19509032201612866f, 0.9807852804032303f},
+    {-1.8369701987210297e-16f, 1.0f},
+    {0.1950903220161283f, 0.9807852804032304f},
+    {0.38268343236509f, 0.9238795325112866f},
+    {0.5555702330196018f, 0.8314696123025455f},
+    {0.7071067811865474f, 0.7071067811865477f},
+    {0.8314696123025452f, 0.5555702330196022f},
+    {0.9238795325112865f, 0.3826834323650904f},
+    {0.9807852804032303f, 0.19509032201612872f},
+};
+
+// twiddle multiply by e^{-j 2 pi K / 32} with K known at compile time (trivial twiddles become swaps)
+template <int K>
+__device__ __forceinline__ float2 tw32(float2 d) {
+    constexpr int k = K & 31;
+    if constexpr (k == 0) return d;
+    if constexpr (k == 8) return make_float2(d.y, -d.x);           // * (-j)
+    if constexpr (k == 16) return make_float2(-d.x, -d.y);         // * (-1)
+    if constexpr (k == 24) return make_float2(-d.y, d.x);          // * (+j)
+    return make_float2(d.x * kTw32[k].c - d.y * kTw32[k].s, d.x * kTw32[k].s + d.y * kTw32[k].c);
+}
+
+// In-register radix-2 DIF DFT of R points; output a[i] = DFT[bitrev_R(i)].  Twiddles are compile-time constants.
+template <int R, int H>
+struct DifStage {
+    template <int S0, int T>
+    static __device__ __forceinline__ void bfly(float2 (&a)[R]) {
+        if constexpr (T < H) {
+            const float2 u = a[S0 + T], v = a[S0 + T + H];
+            a[S0 + T] = make_float2(u.x + v.x, u.y + v.y);
+            a[S0 + T + H] = tw32<T * (32 / (2 * H))>(make_float2(u.x - v.x, u.y - v.y));
+            bfly<S0, T + 1>(a);
         }
     }
+    template <int S0>
+    static __device__ __forceinline__ void blocks(float2 (&a)[R]) {
+        if constexpr (S0 < R) {
+            bfly<S0, 0>(a);
+            blocks<S0 + 2 * H>(a);
+        }
+    }
+    static __device__ __forceinline__ void run(float2 (&a)[R]) {
+        if constexpr (H >= 1) {
+            blocks<0>(a);
+            DifStage<R, H / 2>::run(a);
+        }
+    }
+};
+template <int R>
+struct DifStage<R, 0> {
+    static __device__ __forceinline__ void run(float2 (&)[R]) {}
+};
+
+template <int R>
+__device__ __forceinline__ void dft_dif(float2 (&a)[R], const float2* __restrict__, int) {
+    DifStage<R, R / 2>::run(a);
 }
 
 template <int R>
