@@ -511,3 +511,34 @@ def test_streaming_submit_matches_device_path():
     for od, os_ in outs:
         assert np.array_equal(od.numpy(), ref_d) and np.array_equal(os_.numpy(), ref_s)
     plan.close()
+
+
+@pytest.mark.parametrize("method", ["srp", "both"])
+def test_cuda_graph_capture_replay(method):
+    """svdphat_localize is graph-capturable (no allocation or host sync; BOTH forks/joins internal streams):
+    capture one call with torch.cuda.graph, replay it on new audio, compare with eager calls."""
+    w = make(5, 512)
+    plan = _plan(w, max_frames=256)
+    F = 256
+    a0 = torch.from_numpy(w.audio).to(DEV)
+    n_out = 2 * F if method == "both" else F
+    d = torch.empty(n_out, dtype=torch.int32, device=DEV)
+    sc = torch.empty(n_out, dtype=torch.float32, device=DEV)
+    src = torch.empty_like(a0)
+    src.copy_(a0)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        plan.localize(method, src, F, w.channel_stride, w.frame_stride, d, sc, s.cuda_stream)   # warm-up
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=s):
+        plan.localize(method, src, F, w.channel_stride, w.frame_stride, d, sc, s.cuda_stream)
+    for off in (0, 256):
+        src.copy_(torch.roll(a0, -off * w.hop, dims=1))
+        g.replay()
+        torch.cuda.synchronize()
+        qg, sg = d.cpu().numpy().copy(), sc.cpu().numpy().copy()
+        plan.localize(method, src, F, w.channel_stride, w.frame_stride, d, sc, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        assert np.array_equal(qg, d.cpu().numpy()) and np.array_equal(sg, sc.cpu().numpy())
+    plan.close()

@@ -71,6 +71,27 @@ def run(cfg):
             lat.append(e0.elapsed_time(e1))
         out["call_latency_ms_p50"] = float(np.percentile(lat, 50))
         out["call_latency_ms_p99"] = float(np.percentile(lat, 99))
+        # the same call captured once as a CUDA graph and replayed (streaming deployment: new audio is written
+        # into a fixed device window before each replay)
+        n = calls[0][1]
+        s2 = torch.cuda.Stream()
+        src = audio.clone()
+        with torch.cuda.stream(s2):
+            plan.localize("both", src, n, w.channel_stride, w.frame_stride, d, sc, s2.cuda_stream)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g, stream=s2):
+            plan.localize("both", src, n, w.channel_stride, w.frame_stride, d, sc, s2.cuda_stream)
+        glat = []
+        for _ in range(200):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            glat.append(e0.elapsed_time(e1))
+        out["call_latency_graph_ms_p50"] = float(np.percentile(glat, 50))
+        out["call_latency_graph_ms_p99"] = float(np.percentile(glat, 99))
     plan.close()
     return out
 
