@@ -393,6 +393,8 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
         }
     }
     SVD_CUDA_TRY(gemm_set_attributes());
+    SVD_CUDA_TRY(stft_set_attributes());
+    SVD_CUDA_TRY(topk_set_attributes());
     if ((p.methods & SVDPHAT_METHOD_BOTH) == SVDPHAT_METHOD_BOTH) {
         int lo = 0, hi = 0;
         SVD_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));

@@ -336,15 +336,13 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+cudaError_t topk_set_attributes() {   // per device, at plan creation
+    return cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 49152 * (int)sizeof(float));
+}
+
 cudaError_t launch_topk(const Plan& p, int F, int k, float cos_sep, cudaStream_t s) {
     if (F <= 0) return cudaSuccess;
-    const size_t smem = (size_t)p.Q_eff * sizeof(float);
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && smem > attr) {
-        cudaError_t e = cudaFuncSetAttribute(topk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-        attr = smem;
-    }
+    const size_t smem = (size_t)p.Q_eff * sizeof(float);   // <= 192 KB (Q_classes <= 49152, checked by the API)
     topk_kernel<<<F, 256, smem, s>>>(p.d_S, p.Q_pad, p.Q_eff, F, p.d_dirs, k, cos_sep, p.d_cls);
     return cudaGetLastError();
 }

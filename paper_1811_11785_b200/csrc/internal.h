@@ -147,7 +147,9 @@ cudaError_t launch_finalize(const Plan& p, int method, int F, int32_t* const doa
 // multi-source: greedy top-k with angular suppression over d_S -> class lists, then Y_q of each peak
 cudaError_t launch_topk(const Plan& p, int F, int k, float cos_sep, cudaStream_t s);
 cudaError_t launch_finalize_topk(const Plan& p, int F, int k, int32_t* doa, float* score, cudaStream_t s);
-cudaError_t gemm_set_attributes();
+cudaError_t gemm_set_attributes();   // per-device kernel attributes, set at plan creation
+cudaError_t stft_set_attributes();
+cudaError_t topk_set_attributes();
 
 // setup (float64, device)
 svdphat_status setup_srp_operand(Plan& p, const double* d_tau_cls);

@@ -286,13 +286,6 @@ static cudaError_t launch_rb(const Plan& p, const float* audio, int64_t cs, int6
     const int H = 32 * R;
     const int wbuf = (R * 34 > H + H / 32 + 2) ? R * 34 : H + H / 32 + 2;
     const size_t smem = STFT_WARPS * wbuf * sizeof(float2) + (size_t)p.L.n_chunks * (STFT_WARPS * 16 + 16);
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(stft_phat_kernel<R, BPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             200 * 1024);
-        if (e != cudaSuccess) return e;
-        attr_done = true;
-    }
     dim3 grid((F + STFT_WARPS - 1) / STFT_WARPS, p.M);
     stft_phat_kernel<R, BPC><<<grid, 32 * STFT_WARPS, smem, s>>>(audio, cs, fstride, F, p.L.Mi, p.F_pad, p.d_window,
                                                                  p.d_twN, p.d_P16, p.L.n_chunks, p.k_lo, p.k_hi,
@@ -303,6 +296,23 @@ static cudaError_t launch_rb(const Plan& p, const float* audio, int64_t cs, int6
 template <int R>
 static cudaError_t launch_r(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F, cudaStream_t s) {
     return p.L.bpc == 4 ? launch_rb<R, 4>(p, audio, cs, fstride, F, s) : launch_rb<R, 2>(p, audio, cs, fstride, F, s);
+}
+
+// per device: called by plan creation (cudaFuncSetAttribute applies to the current device only)
+cudaError_t stft_set_attributes() {
+    const int mx = 200 * 1024;
+    cudaError_t e = cudaSuccess;
+#define SVD_STFT_ATTR(R)                                                                                          \
+    if ((e = cudaFuncSetAttribute(stft_phat_kernel<R, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx))) return e; \
+    if ((e = cudaFuncSetAttribute(stft_phat_kernel<R, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx))) return e;
+    SVD_STFT_ATTR(1)
+    SVD_STFT_ATTR(2)
+    SVD_STFT_ATTR(4)
+    SVD_STFT_ATTR(8)
+    SVD_STFT_ATTR(16)
+    SVD_STFT_ATTR(32)
+#undef SVD_STFT_ATTR
+    return e;
 }
 
 cudaError_t launch_stft_phat(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F,
