@@ -460,22 +460,32 @@ static svdphat_status localize_impl(Plan& p, int32_t method, const float* d_audi
         SVD_CUDA_TRY(cudaStreamWaitEvent(sr, p.ev_fork, 0));
         SVD_CUDA_TRY(cudaStreamWaitEvent(sv, p.ev_fork, 0));
     }
-    if (method & SVDPHAT_METHOD_SRP)
+    int32_t* const doas[2] = {doa_srp, doa_svd};
+    float* const scores[2] = {sc_srp, sc_svd};
+    if (method & SVDPHAT_METHOD_SRP) {
         SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_GEMM, sr, [&] { return launch_gemm(p, 0, F, sr); }));
+        // forked: the SRP half of the finalize runs on the SRP stream while the SVD chain is still busy
+        if (fork)
+            SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_FINALIZE, sr,
+                                [&] { return launch_finalize(p, SVDPHAT_METHOD_SRP, F, doas, scores, sr); }));
+    }
     if (method & SVDPHAT_METHOD_SVD) {
         SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_PROJ, sv, [&] { return launch_gemm(p, 1, F, sv); }));
         SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_NORM, sv, [&] { return launch_zsplit(p, F, sv); }));
         SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_SEARCH, sv, [&] { return launch_gemm(p, 2, F, sv); }));
+        if (fork)
+            SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_FINALIZE, sv,
+                                [&] { return launch_finalize(p, SVDPHAT_METHOD_SVD, F, doas, scores, sv); }));
     }
     if (fork) {
         SVD_CUDA_TRY(cudaEventRecord(p.ev_join, sr));
         SVD_CUDA_TRY(cudaEventRecord(p.ev_join2, sv));
         SVD_CUDA_TRY(cudaStreamWaitEvent(s, p.ev_join, 0));
         SVD_CUDA_TRY(cudaStreamWaitEvent(s, p.ev_join2, 0));
+    } else {
+        SVD_CUDA_TRY(
+            staged(p, SVDPHAT_STAGE_FINALIZE, s, [&] { return launch_finalize(p, method, F, doas, scores, s); }));
     }
-    int32_t* const doas[2] = {doa_srp, doa_svd};
-    float* const scores[2] = {sc_srp, sc_svd};
-    SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_FINALIZE, s, [&] { return launch_finalize(p, method, F, doas, scores, s); }));
     p.last_frames = F;
     p.last_method = method;
     return SVDPHAT_OK;

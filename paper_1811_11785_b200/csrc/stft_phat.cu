@@ -151,10 +151,21 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
     if (live) {
         const float* x = audio + (int64_t)m * cs + (int64_t)f * fstride;
         float2 a[R];
+        const float2* win2 = reinterpret_cast<const float2*>(win);
+        if ((reinterpret_cast<uintptr_t>(x) & 7) == 0) {             // 8-byte aligned frame: float2 loads
+            const float2* x2 = reinterpret_cast<const float2*>(x);
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int n2 = 2 * (lane + 32 * r);
-            a[r] = make_float2(__ldg(x + n2) * __ldg(win + n2), __ldg(x + n2 + 1) * __ldg(win + n2 + 1));
+            for (int r = 0; r < R; ++r) {
+                const float2 v = __ldg(x2 + lane + 32 * r), wv = __ldg(win2 + lane + 32 * r);
+                a[r] = make_float2(v.x * wv.x, v.y * wv.y);
+            }
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                const int n2 = 2 * (lane + 32 * r);
+                const float2 wv = __ldg(win2 + lane + 32 * r);
+                a[r] = make_float2(__ldg(x + n2) * wv.x, __ldg(x + n2 + 1) * wv.y);
+            }
         }
         // pass 1: DFT over r, twiddle W_H^{lane k1}, transpose S[k1][lane]
         dft_dif<R>(a, twN, N);
@@ -224,13 +235,13 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
     __syncthreads();
 
     // ---- coalesced write-out: per chunk, 8 frames x unit_bytes contiguous at P16[c][m][f0..f0+7]
-    const int unit_bytes = bpc * 4;
-    const int words_per_chunk = STFT_WARPS * unit_bytes / 4;
-    const int total = n_chunks * words_per_chunk;
+    constexpr int unit_bytes = BPC * 4;
+    constexpr int vec_per_chunk = STFT_WARPS * unit_bytes / 16;      // 16-byte stores: 8 (bpc 4) or 4 (bpc 2)
+    const int total = n_chunks * vec_per_chunk;
     for (int i = threadIdx.x; i < total; i += blockDim.x) {
-        const int cc = i / words_per_chunk, wi = i % words_per_chunk;
-        uint32_t* out = reinterpret_cast<uint32_t*>(P16 + (((int64_t)cc * Mi + m) * F_pad + f0) * unit_bytes);
-        out[wi] = reinterpret_cast<const uint32_t*>(tile + cc * tile_stride)[wi];
+        const int cc = i / vec_per_chunk, wi = i % vec_per_chunk;
+        uint4* out = reinterpret_cast<uint4*>(P16 + (((int64_t)cc * Mi + m) * F_pad + f0) * unit_bytes);
+        out[wi] = reinterpret_cast<const uint4*>(tile + cc * tile_stride)[wi];
     }
 }
 

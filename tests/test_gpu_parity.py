@@ -542,3 +542,23 @@ def test_cuda_graph_capture_replay(method):
         torch.cuda.synchronize()
         assert np.array_equal(qg, d.cpu().numpy()) and np.array_equal(sg, sc.cpu().numpy())
     plan.close()
+
+
+def test_odd_strides_same_results():
+    """Channel stride L+1 (odd): half the channels' frames are not 8-byte aligned (scalar-load path of the STFT);
+    results must equal the packed layout's."""
+    w = make(1)
+    plan = _plan(w)
+    F, L = w.n_frames, w.audio.shape[1]
+    a = torch.from_numpy(w.audio).to(DEV)
+    b = torch.zeros((w.M, L + 1), dtype=torch.float32, device=DEV)
+    b[:, :L] = a
+    d1 = torch.empty(2 * F, dtype=torch.int32, device=DEV)
+    s1 = torch.empty(2 * F, dtype=torch.float32, device=DEV)
+    d2, s2 = torch.empty_like(d1), torch.empty_like(s1)
+    st = torch.cuda.current_stream().cuda_stream
+    plan.localize("both", a, F, L, w.hop, d1, s1, st)
+    plan.localize("both", b, F, L + 1, w.hop, d2, s2, st)
+    torch.cuda.synchronize()
+    assert torch.equal(d1, d2) and torch.equal(s1, s2)
+    plan.close()
