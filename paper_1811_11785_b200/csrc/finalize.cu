@@ -56,6 +56,78 @@ __global__ void zsplit_kernel(float* __restrict__ Z, int F, int64_t F_pad, int l
     }
 }
 
+// The same, one 128-thread CTA per frame with the frame's Z held in registers (NV float4 per thread, ldz <= 512 NV):
+// every partial is read once with 16-byte loads, all NV x nsplit loads of a thread in flight together.
+constexpr int ZS_THREADS = 128;
+template <int NV>
+__global__ void __launch_bounds__(ZS_THREADS)
+    zsplit_cta_kernel(float* __restrict__ Z, int64_t F_pad, int ldz, int nsplit, __half* __restrict__ Zs, int K2,
+                      int* __restrict__ zflag) {
+    __shared__ float s_ss[ZS_THREADS / 32];
+    const int f = blockIdx.x;
+    const int t = threadIdx.x;
+    const int n4 = ldz >> 2;
+    float4* z = reinterpret_cast<float4*>(Z + (int64_t)f * ldz);
+    const int64_t split4 = F_pad * (int64_t)n4;
+    float4 v[NV];
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const int i = t + ZS_THREADS * j;
+        v[j] = i < n4 ? z[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    for (int sp = 1; sp < nsplit; ++sp) {
+        float4 w[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const int i = t + ZS_THREADS * j;
+            w[j] = i < n4 ? z[sp * split4 + i] : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            v[j].x += w[j].x;
+            v[j].y += w[j].y;
+            v[j].z += w[j].z;
+            v[j].w += w[j].w;
+        }
+    }
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const int i = t + ZS_THREADS * j;
+        if (i < n4) {
+            if (nsplit > 1) z[i] = v[j];                  // the summed Z stays readable (debug dump)
+            ss += v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+    if ((t & 31) == 0) s_ss[t >> 5] = ss;
+    __syncthreads();
+    ss = 0.f;
+#pragma unroll
+    for (int w = 0; w < ZS_THREADS / 32; ++w) ss += s_ss[w];   // same order in every thread
+    const float inv = ss > 0.f ? rsqrtf(ss) : 0.f;
+    if (t == 0) zflag[f] = ss > 0.f ? 0 : 1;
+    uint2* out = reinterpret_cast<uint2*>(Zs + (int64_t)f * K2);     // 4 halves per store
+#pragma unroll
+    for (int j = 0; j < NV; ++j) {
+        const int i = t + ZS_THREADS * j;
+        if (i < n4) {
+            const float a[4] = {v[j].x * inv, v[j].y * inv, v[j].z * inv, v[j].w * inv};
+            __half hi[4], lo[4];
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+                hi[e] = __float2half_rn(a[e]);
+                lo[e] = __float2half_rn(a[e] - __half2float(hi[e]));
+            }
+            const uint2 h = *reinterpret_cast<const uint2*>(hi), l = *reinterpret_cast<const uint2*>(lo);
+            out[i] = h;
+            out[n4 + i] = h;
+            out[2 * n4 + i] = l;
+        }
+    }
+}
+
 // CTA = 32 consecutive frames (lane = frame, so every phasor record load is a coalesced 512-byte row) x 8 warps
 // striding over the bin chunks; partial sums meet in shared memory.
 constexpr int FIN_WARPS = 8;
@@ -72,7 +144,7 @@ struct FinOut {
 };
 
 template <int NM>
-__global__ void __launch_bounds__(32 * FIN_WARPS)
+__global__ void __launch_bounds__(32 * FIN_WARPS, 3)
     finalize_kernel(FinOut o, const uint8_t* __restrict__ P16, int F, int64_t F_pad, int M, int Mi, int bpc,
                     int n_chunks, int Kb, int N, const int* __restrict__ rep, const float* __restrict__ delay) {
     static_assert(NM >= 1 && NM <= 4, "1..4 results per frame");
@@ -110,43 +182,50 @@ __global__ void __launch_bounds__(32 * FIN_WARPS)
 #pragma unroll
                 for (int t = 0; t < 4; ++t) ar[j][t] = ai[j][t] = 0.f;
             const int kb0 = cc * bpc;
-            for (int m = 0; m < M; ++m) {
-                const uint8_t* rec = P16 + (((int64_t)cc * Mi + m) * F_pad + f) * ub;
-                float er[4], ei[4];
-                if (bpc == 4) {
-                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(rec));
-                    const float2 r01 = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
-                    const float2 r23 = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
-                    const float2 i01 = __half22float2(*reinterpret_cast<const __half2*>(&v.z));
-                    const float2 i23 = __half22float2(*reinterpret_cast<const __half2*>(&v.w));
-                    er[0] = r01.x; er[1] = r01.y; er[2] = r23.x; er[3] = r23.y;
-                    ei[0] = i01.x; ei[1] = i01.y; ei[2] = i23.x; ei[3] = i23.y;
-                } else {
-                    const uint2 v = __ldg(reinterpret_cast<const uint2*>(rec));
-                    const float2 r01 = __half22float2(*reinterpret_cast<const __half2*>(&v.x));
-                    const float2 i01 = __half22float2(*reinterpret_cast<const __half2*>(&v.y));
-                    er[0] = r01.x; er[1] = r01.y; ei[0] = i01.x; ei[1] = i01.y;
-                    er[2] = er[3] = ei[2] = ei[3] = 0.f;
+            // mics in groups of 4: the group's records and delays are loaded before any of them is used
+            for (int m0 = 0; m0 < M; m0 += 4) {
+                uint4 v[4];
+                float dl[NM][4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int m = m0 + u < M ? m0 + u : M - 1;
+                    const uint8_t* rec = P16 + (((int64_t)cc * Mi + m) * F_pad + f) * ub;
+                    if (bpc == 4) {
+                        v[u] = __ldg(reinterpret_cast<const uint4*>(rec));
+                    } else {
+                        const uint2 w2 = __ldg(reinterpret_cast<const uint2*>(rec));
+                        v[u] = make_uint4(w2.x, 0u, w2.y, 0u);      // [re01 | 0 | im01 | 0]: same slots as bpc 4
+                    }
+#pragma unroll
+                    for (int j = 0; j < NM; ++j) dl[j][u] = __ldg(dq[j] + m);
                 }
 #pragma unroll
-                for (int t = 0; t < 4; ++t)
-                    if (t < bpc && (er[t] != 0.f || ei[t] != 0.f)) nk[t] += 1;
+                for (int u = 0; u < 4; ++u) {
+                    if (m0 + u >= M) break;
+                    const float2 r01 = __half22float2(*reinterpret_cast<const __half2*>(&v[u].x));
+                    const float2 r23 = __half22float2(*reinterpret_cast<const __half2*>(&v[u].y));
+                    const float2 i01 = __half22float2(*reinterpret_cast<const __half2*>(&v[u].z));
+                    const float2 i23 = __half22float2(*reinterpret_cast<const __half2*>(&v[u].w));
+                    const float er[4] = {r01.x, r01.y, r23.x, r23.y}, ei[4] = {i01.x, i01.y, i23.x, i23.y};
 #pragma unroll
-                for (int j = 0; j < NM; ++j) {
-                    // e^{+j 2 pi k delta_m / N} for k = kb0 .. kb0+bpc-1: base rotation, then unit steps
-                    const float dl = __ldg(dq[j] + m);
-                    float bs, bc, ss, sc;
-                    sincospi_fast((float)kb0 * dl * inv2N, &bs, &bc);
-                    sincospi_fast(dl * inv2N, &ss, &sc);
+                    for (int t = 0; t < 4; ++t)
+                        if (t < bpc && (er[t] != 0.f || ei[t] != 0.f)) nk[t] += 1;
 #pragma unroll
-                    for (int t = 0; t < 4; ++t) {
-                        if (t < bpc) {
-                            ar[j][t] += er[t] * bc - ei[t] * bs;
-                            ai[j][t] += er[t] * bs + ei[t] * bc;
+                    for (int j = 0; j < NM; ++j) {
+                        // e^{+j 2 pi k delta_m / N} for k = kb0 .. kb0+bpc-1: base rotation, then unit steps
+                        float bs, bc, ss, sc;
+                        sincospi_fast((float)kb0 * dl[j][u] * inv2N, &bs, &bc);
+                        sincospi_fast(dl[j][u] * inv2N, &ss, &sc);
+#pragma unroll
+                        for (int t = 0; t < 4; ++t) {
+                            if (t < bpc) {
+                                ar[j][t] += er[t] * bc - ei[t] * bs;
+                                ai[j][t] += er[t] * bs + ei[t] * bc;
+                            }
+                            const float nb = bc * sc - bs * ss;
+                            bs = bs * sc + bc * ss;
+                            bc = nb;
                         }
-                        const float nb = bc * sc - bs * ss;
-                        bs = bs * sc + bc * ss;
-                        bc = nb;
                     }
                 }
             }
@@ -210,10 +289,22 @@ cudaError_t launch_split_argmax(const Plan& p, int F, int S, cudaStream_t s) {
 
 cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s) {
     if (F <= 0) return cudaSuccess;
+    const int ldz = 2 * p.Dh, S = proj_shape(p, F).ksplit;
+    if (ldz % 4 == 0 && ldz <= 4 * ZS_THREADS * 8) {
+        const int nv = (ldz / 4 + ZS_THREADS - 1) / ZS_THREADS;
+        if (nv <= 1)
+            zsplit_cta_kernel<1><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag);
+        else if (nv <= 2)
+            zsplit_cta_kernel<2><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag);
+        else if (nv <= 4)
+            zsplit_cta_kernel<4><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag);
+        else
+            zsplit_cta_kernel<8><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag);
+        return cudaGetLastError();
+    }
     const int threads = 256;
     const int blocks = (F * 32 + threads - 1) / threads;
-    zsplit_kernel<<<blocks, threads, 0, s>>>(p.d_Z32, F, p.F_pad, 2 * p.Dh, proj_shape(p, F).ksplit, p.d_Zs16, p.K2,
-                                             p.d_zflag);
+    zsplit_kernel<<<blocks, threads, 0, s>>>(p.d_Z32, F, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag);
     return cudaGetLastError();
 }
 

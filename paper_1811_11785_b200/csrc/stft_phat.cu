@@ -136,7 +136,7 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
     constexpr int Kb = H + 1;
     constexpr int G = 32 / R;                     // lanes per 32-point DFT in pass 2 (R <= 32)
     constexpr int SROW = 34;                      // padded row (float2) of the pass-1 transpose S[k1][l]
-    constexpr int WBUF = (R * SROW > H + H / 32 + 2) ? R * SROW : H + H / 32 + 2;   // float2 per warp
+    constexpr int WBUF = (R * SROW > H + H / 16 + 2) ? R * SROW : H + H / 16 + 2;   // float2 per warp (even)
     extern __shared__ __align__(16) uint8_t sm[];
     float2* wbuf = reinterpret_cast<float2*>(sm) + (threadIdx.x >> 5) * WBUF;
     const int tile_stride = STFT_WARPS * 16 + 16;                                    // padded chunk row (bytes)
@@ -148,8 +148,9 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
     const int f = f0 + warp;
     const bool live = f < F;
 
-    if (live) {
-        const float* x = audio + (int64_t)m * cs + (int64_t)f * fstride;
+    {   // every warp runs the FFT (a dead warp re-reads frame F-1 and discards it), so the shuffles below are not
+        // inside divergent code and compile without WARPSYNC/collective fix-ups
+        const float* x = audio + (int64_t)m * cs + (int64_t)(live ? f : F - 1) * fstride;
         float2 a[R];
         const float2* win2 = reinterpret_cast<const float2*>(win);
         if ((reinterpret_cast<uintptr_t>(x) & 7) == 0) {             // 8-byte aligned frame: float2 loads
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
                 }
             }
         }
-        // Z[k1 + R (a + R bitrev_G(h))] -> natural order, padded by one float2 per 32
+        // Z[k1 + R (a + R bitrev_G(h))] -> natural order, padded by two float2 per 32 (keeps 16-byte alignment)
         int bg = 0;
         {
             int lg = 0;
@@ -208,29 +209,86 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
 #pragma unroll
         for (int i = 0; i < R; ++i) {
             const int k = k1 + R * (bitrev_r<R>(i) + R * bg);
-            wbuf[k + (k >> 5)] = a[i];
+            wbuf[k + 2 * (k >> 5)] = a[i];
         }
         __syncwarp();
     }
 
-    // ---- real-FFT post pass + PHAT per bin (lanes over consecutive bins), halves into the padded record tile
-    for (int k = lane; k < n_chunks * bpc; k += 32) {
-        float2 e = make_float2(0.f, 0.f);
-        // bins outside the band [k_lo, k_hi) or masked out for this frame contribute nothing (NEXT-3)
-        if (live && k < Kb && k >= k_lo && k < k_hi && (!mask || mask[(int64_t)f * mask_stride + k])) {
-            const int k0 = k & (H - 1), km = (H - k) & (H - 1);
-            const float2 Zk = wbuf[k0 + (k0 >> 5)];
-            const float2 Zm = wbuf[km + (km >> 5)];
-            const float2 Zr = make_float2(Zm.x, -Zm.y);                                  // conj(Z[H-k])
-            const float2 E = make_float2(0.5f * (Zk.x + Zr.x), 0.5f * (Zk.y + Zr.y));
-            const float2 Dd = make_float2(0.5f * (Zk.x - Zr.x), 0.5f * (Zk.y - Zr.y));
-            const float2 t = cmul(__ldg(twN + k), Dd);                                   // w^k (Z - Zr)/2
-            e = phat(make_float2(E.x + t.y, E.y - t.x));                                // E - j t
+    // ---- real-FFT post pass + PHAT: one lane per record (BPC consecutive bins), 2X = (Z_k + conj Z_{H-k}) -
+    // j w^k (Z_k - conj Z_{H-k}) (the factor 1/2 is dropped: PHAT is scale-invariant and 2 is exact), one 16- or
+    // 8-byte shared store per record.  Bin H (Nyquist) = Re Z_0 - Im Z_0 is the lone bin of the last record.
+    {
+        constexpr int NREC = H / BPC;                                   // records of bins 0..H-1
+        const bool filter = (k_lo > 0) || (k_hi < Kb) || (mask != nullptr);
+        for (int c = lane; c < NREC; c += 32) {
+            float re[BPC], im[BPC];
+            if (live) {
+                const int k0 = c * BPC;
+                const float2* zk = wbuf + k0 + 2 * (k0 >> 5);            // BPC consecutive bins, 16-byte aligned
+                float2 Zk[BPC], tw[BPC];
+                if constexpr (BPC == 4) {
+                    const float4 z01 = *reinterpret_cast<const float4*>(zk);
+                    const float4 z23 = *reinterpret_cast<const float4*>(zk + 2);
+                    Zk[0] = make_float2(z01.x, z01.y); Zk[1] = make_float2(z01.z, z01.w);
+                    Zk[2] = make_float2(z23.x, z23.y); Zk[3] = make_float2(z23.z, z23.w);
+                    const float4 t01 = __ldg(reinterpret_cast<const float4*>(twN + k0));
+                    const float4 t23 = __ldg(reinterpret_cast<const float4*>(twN + k0 + 2));
+                    tw[0] = make_float2(t01.x, t01.y); tw[1] = make_float2(t01.z, t01.w);
+                    tw[2] = make_float2(t23.x, t23.y); tw[3] = make_float2(t23.z, t23.w);
+                } else {
+                    const float4 z01 = *reinterpret_cast<const float4*>(zk);
+                    Zk[0] = make_float2(z01.x, z01.y); Zk[1] = make_float2(z01.z, z01.w);
+                    const float4 t01 = __ldg(reinterpret_cast<const float4*>(twN + k0));
+                    tw[0] = make_float2(t01.x, t01.y); tw[1] = make_float2(t01.z, t01.w);
+                }
+#pragma unroll
+                for (int s2 = 0; s2 < BPC; ++s2) {
+                    const int km = (H - k0 - s2) & (H - 1);
+                    const float2 Zm = wbuf[km + 2 * (km >> 5)];
+                    const float Ex = Zk[s2].x + Zm.x, Ey = Zk[s2].y - Zm.y;              // Z_k + conj Z_{H-k}
+                    const float Dx = Zk[s2].x - Zm.x, Dy = Zk[s2].y + Zm.y;              // Z_k - conj Z_{H-k}
+                    const float tx = tw[s2].x * Dx - tw[s2].y * Dy, ty = tw[s2].x * Dy + tw[s2].y * Dx;
+                    const float2 e = phat(make_float2(Ex + ty, Ey - tx));                   // E - j t
+                    re[s2] = e.x;
+                    im[s2] = e.y;
+                }
+                if (filter) {            // bins outside [k_lo, k_hi) or masked out contribute nothing (NEXT-3)
+#pragma unroll
+                    for (int s2 = 0; s2 < BPC; ++s2) {
+                        const int k = k0 + s2;
+                        if (k < k_lo || k >= k_hi || (mask && !mask[(int64_t)f * mask_stride + k])) re[s2] = im[s2] = 0.f;
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int s2 = 0; s2 < BPC; ++s2) re[s2] = im[s2] = 0.f;
+            }
+            uint8_t* rec = tile + c * tile_stride + warp * (BPC * 4);
+            if constexpr (BPC == 4) {
+                const __half2 h0 = __floats2half2_rn(re[0], re[1]), h1 = __floats2half2_rn(re[2], re[3]);
+                const __half2 h2 = __floats2half2_rn(im[0], im[1]), h3 = __floats2half2_rn(im[2], im[3]);
+                *reinterpret_cast<uint4*>(rec) = make_uint4(*reinterpret_cast<const uint32_t*>(&h0),
+                                                            *reinterpret_cast<const uint32_t*>(&h1),
+                                                            *reinterpret_cast<const uint32_t*>(&h2),
+                                                            *reinterpret_cast<const uint32_t*>(&h3));
+            } else {
+                const __half2 h0 = __floats2half2_rn(re[0], re[1]), h1 = __floats2half2_rn(im[0], im[1]);
+                *reinterpret_cast<uint2*>(rec) = make_uint2(*reinterpret_cast<const uint32_t*>(&h0),
+                                                            *reinterpret_cast<const uint32_t*>(&h1));
+            }
         }
-        const int cc = k / BPC, s = k % BPC;
-        __half* rec = reinterpret_cast<__half*>(tile + cc * tile_stride + warp * (BPC * 4));
-        rec[s] = __float2half_rn(e.x);
-        rec[bpc + s] = __float2half_rn(e.y);
+        if (lane == 0) {                                                // record NREC: bin H, zero padding after it
+            float e = 0.f;
+            if (live && H >= k_lo && H < k_hi && (!mask || mask[(int64_t)f * mask_stride + H])) {
+                const float2 Z0 = wbuf[0];
+                const float v = Z0.x - Z0.y;
+                e = v > 0.f ? 1.f : (v < 0.f ? -1.f : 0.f);
+            }
+            __half* rec = reinterpret_cast<__half*>(tile + NREC * tile_stride + warp * (BPC * 4));
+#pragma unroll
+            for (int s2 = 0; s2 < 2 * BPC; ++s2) rec[s2] = __float2half_rn(0.f);
+            rec[0] = __float2half_rn(e);
+        }
     }
     __syncthreads();
 
@@ -295,7 +353,7 @@ __global__ void stft_phat_small_kernel(const float* __restrict__ audio, int64_t 
 template <int R, int BPC>
 static cudaError_t launch_rb(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F, cudaStream_t s) {
     const int H = 32 * R;
-    const int wbuf = (R * 34 > H + H / 32 + 2) ? R * 34 : H + H / 32 + 2;
+    const int wbuf = (R * 34 > H + H / 16 + 2) ? R * 34 : H + H / 16 + 2;
     const size_t smem = STFT_WARPS * wbuf * sizeof(float2) + (size_t)p.L.n_chunks * (STFT_WARPS * 16 + 16);
     dim3 grid((F + STFT_WARPS - 1) / STFT_WARPS, p.M);
     stft_phat_kernel<R, BPC><<<grid, 32 * STFT_WARPS, smem, s>>>(audio, cs, fstride, F, p.L.Mi, p.F_pad, p.d_window,

@@ -1,0 +1,6 @@
+#!/bin/bash
+# Full GPU parity suite + a short contract bench (dev loop)
+export PYTHONPATH=$PWD
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -q -x > gpurun_out/check_tests.log 2>&1; echo "exit $?" >> gpurun_out/check_tests.log
+timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/check_b3.jsonl 2>gpurun_out/check_b3.err
