@@ -128,9 +128,12 @@ __global__ void __launch_bounds__(ZS_THREADS)
     }
 }
 
-// CTA = 32 consecutive frames (lane = frame, so every phasor record load is a coalesced 512-byte row) x 8 warps
-// striding over the bin chunks; partial sums meet in shared memory.
+// CTA = 8 consecutive frames x 8 warps; lane = (chunk sub-slot lane>>3, frame lane&7), so a warp's record loads are
+// four coalesced 128-byte rows and the 32 chunk slots of the CTA stride over the bin chunks; partial sums meet in
+// shared memory (fixed order: deterministic).  8 frames per CTA keeps ~F/8 CTAs in flight (all SMs busy at 10^4).
 constexpr int FIN_WARPS = 8;
+constexpr int FIN_FRAMES = 8;
+constexpr int FIN_SLOTS = FIN_WARPS * (32 / FIN_FRAMES);
 // One or two methods per launch: method slot j in [0, nm) reads keys[j] and writes doa[j]/score[j]; the phasor
 // records of the frame are read once for both.
 struct FinOut {
@@ -148,10 +151,11 @@ __global__ void __launch_bounds__(32 * FIN_WARPS, 3)
     finalize_kernel(FinOut o, const uint8_t* __restrict__ P16, int F, int64_t F_pad, int M, int Mi, int bpc,
                     int n_chunks, int Kb, int N, const int* __restrict__ rep, const float* __restrict__ delay) {
     static_assert(NM >= 1 && NM <= 4, "1..4 results per frame");
-    __shared__ float s_y[NM][FIN_WARPS][32];
-    __shared__ int s_p[FIN_WARPS][32];
+    __shared__ float s_y[NM][FIN_SLOTS][FIN_FRAMES];
+    __shared__ int s_p[FIN_SLOTS][FIN_FRAMES];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int f = blockIdx.x * 32 + lane;
+    const int fl = lane % FIN_FRAMES, slot = warp * (32 / FIN_FRAMES) + lane / FIN_FRAMES;
+    const int f = blockIdx.x * FIN_FRAMES + fl;
     const bool valid = f < F;
     int q[NM];
     const float* dq[NM];
@@ -174,7 +178,7 @@ __global__ void __launch_bounds__(32 * FIN_WARPS, 3)
     for (int j = 0; j < NM; ++j) ysum[j] = 0.f;
     int pairs = 0;
     if (valid) {
-        for (int cc = warp; cc < n_chunks; cc += FIN_WARPS) {
+        for (int cc = slot; cc < n_chunks; cc += FIN_SLOTS) {
             float ar[NM][4], ai[NM][4];
             int nk[4] = {0, 0, 0, 0};
 #pragma unroll
@@ -240,18 +244,18 @@ __global__ void __launch_bounds__(32 * FIN_WARPS, 3)
         }
     }
 #pragma unroll
-    for (int j = 0; j < NM; ++j) s_y[j][warp][lane] = ysum[j];
-    s_p[warp][lane] = pairs;
+    for (int j = 0; j < NM; ++j) s_y[j][slot][fl] = ysum[j];
+    s_p[slot][fl] = pairs;
     __syncthreads();
-    if (warp == 0 && valid) {
+    if (slot == 0 && valid) {
         int pr = 0;
-#pragma unroll
-        for (int w = 0; w < FIN_WARPS; ++w) pr += s_p[w][lane];
+#pragma unroll 8
+        for (int w = 0; w < FIN_SLOTS; ++w) pr += s_p[w][fl];
 #pragma unroll
         for (int j = 0; j < NM; ++j) {
             float y = 0.f;
-#pragma unroll
-            for (int w = 0; w < FIN_WARPS; ++w) y += s_y[j][w][lane];
+#pragma unroll 8
+            for (int w = 0; w < FIN_SLOTS; ++w) y += s_y[j][w][fl];
             const bool dead = (pr == 0) || q[j] < 0 || (o.zflag[j] != nullptr && o.zflag[j][f] != 0);
             o.doa[j][(int64_t)f * o.out_stride] = dead ? -1 : q[j];
             o.score[j][(int64_t)f * o.out_stride] = dead ? 0.f : 0.5f * y;
@@ -328,7 +332,7 @@ cudaError_t launch_finalize(const Plan& p, int method, int F, int32_t* const doa
         o.score[nm] = score[1];
         ++nm;
     }
-    const dim3 grid((F + 31) / 32), block(32 * FIN_WARPS);
+    const dim3 grid((F + FIN_FRAMES - 1) / FIN_FRAMES), block(32 * FIN_WARPS);
     if (nm == 2)
         finalize_kernel<2><<<grid, block, 0, s>>>(o, p.d_P16, F, p.F_pad, p.M, p.L.Mi, p.L.bpc, p.L.n_chunks, p.Kb,
                                                   p.N, p.d_rep, p.d_delay);
@@ -350,7 +354,7 @@ cudaError_t launch_finalize_topk(const Plan& p, int F, int k, int32_t* doa, floa
         o.doa[j] = doa + j;
         o.score[j] = score + j;
     }
-    const dim3 grid((F + 31) / 32), block(32 * FIN_WARPS);
+    const dim3 grid((F + FIN_FRAMES - 1) / FIN_FRAMES), block(32 * FIN_WARPS);
 #define SVD_FIN(K)                                                                                                 \
     if (k == K) {                                                                                                  \
         finalize_kernel<K><<<grid, block, 0, s>>>(o, p.d_P16, F, p.F_pad, p.M, p.L.Mi, p.L.bpc, p.L.n_chunks, p.Kb,  \
