@@ -371,9 +371,7 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
 // TMA-loads rows [m*256 + 128r, +128) of A and its 4 producer warps build frames [n*256 + 128r, +128) of B; the
 // even (leader) CTA issues tcgen05.mma.cta_group::2 for both.  Per SM this halves the shared-memory operand
 // traffic of the 1-CTA kernel (ncu r01: ~192 B/clk/SM needed at full MMA rate), the reason for the pair.
-// Warps: 0 TMA (+TMEM alloc), 1 MMA (leader), 2-5 epilogue (lane groups 2,3,0,1), 6-9 producer.  The producer
-// keeps the frame's phasors of the current bin chunk in registers.  (Register double-buffering of the next chunk
-// was tried and removed: the apparent 'load cost' was power - zeroed operands keep the clock high under the cap.)
+// Warps: 0 TMA (+TMEM alloc), 1 MMA (leader), 2-5 epilogue (lane groups 2,3,0,1), 6-9 producer (produce_x_pair).
 // ================================================================================================================
 constexpr int STAGES2 = 6;
 constexpr int A2_BYTES = 128 * BK * 2;                 // 16 KB: this CTA's half of the 256 A rows
@@ -382,13 +380,89 @@ constexpr int NPW2 = 4;                                // producer warps per CTA
 constexpr int THREADS2 = 32 * (6 + NPW2);
 constexpr int SMEM2_BYTES = 1024 + STAGES2 * (A2_BYTES + B2_BYTES) + 256;
 
+// Producer warps of the CTA-pair kernels: this thread's frame row of the cross-spectrum X (eqs. 3, 7, PAPER.md:66,
+// 99) for the bin chunks [w.c0, w.c1) of a work unit, written into the SW128 K-major operand ring sX (stage stride
+// XB bytes, 8 units = one 64-element slab per stage).  The frame's phasors of the current chunk stay in registers.
+// (Register double-buffering of the next chunk was tried and removed: the apparent 'load cost' was power - zeroed
+// operands keep the clock high under the cap.)
+template <int Mi, int BPC, int NSTAGES, int XB>
+__device__ __forceinline__ void produce_x_pair(const GemmParams& p, const Unit& w, int f, bool valid, uint8_t* sX,
+                                               uint64_t* full, uint64_t* empty, int& stage, uint32_t& phase,
+                                               uint32_t row_off, uint32_t xr) {
+    constexpr PairTab<Mi> PT{};
+    constexpr int kPairs = Mi * (Mi - 1) / 2;
+    constexpr int kUnitsRaw = (BPC == 4) ? kPairs : (kPairs + 1) / 2;
+    constexpr int kU = (kUnitsRaw + 7) / 8 * 8;
+    constexpr int kUB = BPC * 4;
+    const int lane = threadIdx.x & 31;
+#pragma unroll 1
+    for (int c = w.c0; c < w.c1; ++c) {
+        uint32_t e[Mi][BPC];
+        const uint8_t* src = p.P16 + ((int64_t)c * Mi * p.F_pad + f) * kUB;
+#pragma unroll
+        for (int m = 0; m < Mi; ++m) {
+            if constexpr (BPC == 4) {
+                uint4 v = valid ? __ldg(reinterpret_cast<const uint4*>(src + (int64_t)m * p.F_pad * kUB))
+                                : make_uint4(0, 0, 0, 0);
+                e[m][0] = v.x;
+                e[m][1] = v.y;
+                e[m][2] = v.z;
+                e[m][3] = v.w;
+            } else {
+                uint2 v = valid ? __ldg(reinterpret_cast<const uint2*>(src + (int64_t)m * p.F_pad * kUB))
+                                : make_uint2(0, 0);
+                e[m][0] = v.x;
+                e[m][1] = v.y;
+            }
+        }
+        uint32_t outw[4];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            if ((u & 7) == 0) mbar_wait(&empty[stage], phase ^ 1);
+            if constexpr (BPC == 4) {
+                if (u < kPairs) {
+                    const int a = PT.i[u], b = PT.j[u];
+                    const uint32_t nra01 = e[a][0] ^ 0x80008000u, nra23 = e[a][1] ^ 0x80008000u;
+                    outw[0] = h2fma(e[a][0], e[b][0], h2mul(e[a][2], e[b][2]));
+                    outw[1] = h2fma(e[a][1], e[b][1], h2mul(e[a][3], e[b][3]));
+                    outw[2] = h2fma(e[a][2], e[b][0], h2mul(nra01, e[b][2]));
+                    outw[3] = h2fma(e[a][3], e[b][1], h2mul(nra23, e[b][3]));
+                } else {
+                    outw[0] = outw[1] = outw[2] = outw[3] = 0u;
+                }
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int pp = 2 * u + h;
+                    if (pp < kPairs) {
+                        const int a = PT.i[pp], b = PT.j[pp];
+                        const uint32_t nra = e[a][0] ^ 0x80008000u;
+                        outw[2 * h + 0] = h2fma(e[a][0], e[b][0], h2mul(e[a][1], e[b][1]));
+                        outw[2 * h + 1] = h2fma(e[a][1], e[b][0], h2mul(nra, e[b][1]));
+                    } else {
+                        outw[2 * h + 0] = outw[2 * h + 1] = 0u;
+                    }
+                }
+            }
+            const uint32_t dst = smem_u32(sX + stage * XB) + row_off + ((((uint32_t)u & 7u) ^ xr) << 4);
+            st_shared_v4(dst, outw[0], outw[1], outw[2], outw[3]);
+            if ((u & 7) == 7) {
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(&full[stage], 0);   // the leader's barrier
+                if (++stage == NSTAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    }
+}
+
 template <int Mi, int BPC, int MODE>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
     constexpr bool kProducer = (MODE != 2);
-    constexpr int kPairs = Mi * (Mi - 1) / 2;
-    constexpr int kUnitsRaw = (BPC == 4) ? kPairs : (kPairs + 1) / 2;
-    constexpr int kU = (kUnitsRaw + 7) / 8 * 8;
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -532,79 +606,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
             }
         }
     } else if (warp >= 6 && kProducer) {
-        constexpr PairTab<Mi> PT{};
         const int tp = (warp - 6) * 32 + lane;                    // frame row of this CTA's half tile: 0..127
         const uint32_t row_off = (uint32_t)((tp >> 3) * 1024 + (tp & 7) * 128);
         const uint32_t xr = (uint32_t)(tp & 7);
         int stage = 0;
         uint32_t phase = 0;
-        constexpr int kUB = BPC * 4;
         for (int t = pair; t < units; t += n_pairs) {
             const Unit w = unit_of(p, t);
             const int f = w.n * bn + (int)rank * hb + tp;
             const bool valid = f < p.F && tp < hb && !(p.dbg & 1);
-#pragma unroll 1
-            for (int c = w.c0; c < w.c1; ++c) {
-                uint32_t e[Mi][BPC];
-                const uint8_t* src = p.P16 + ((int64_t)c * Mi * p.F_pad + f) * kUB;
-#pragma unroll
-                for (int m = 0; m < Mi; ++m) {
-                    if constexpr (BPC == 4) {
-                        uint4 v = valid ? __ldg(reinterpret_cast<const uint4*>(src + (int64_t)m * p.F_pad * kUB))
-                                        : make_uint4(0, 0, 0, 0);
-                        e[m][0] = v.x;
-                        e[m][1] = v.y;
-                        e[m][2] = v.z;
-                        e[m][3] = v.w;
-                    } else {
-                        uint2 v = valid ? __ldg(reinterpret_cast<const uint2*>(src + (int64_t)m * p.F_pad * kUB))
-                                        : make_uint2(0, 0);
-                        e[m][0] = v.x;
-                        e[m][1] = v.y;
-                    }
-                }
-                uint32_t outw[4];
-#pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    if ((u & 7) == 0) mbar_wait(&empty[stage], phase ^ 1);
-                    if constexpr (BPC == 4) {
-                        if (u < kPairs) {
-                            const int a = PT.i[u], b = PT.j[u];
-                            const uint32_t nra01 = e[a][0] ^ 0x80008000u, nra23 = e[a][1] ^ 0x80008000u;
-                            outw[0] = h2fma(e[a][0], e[b][0], h2mul(e[a][2], e[b][2]));
-                            outw[1] = h2fma(e[a][1], e[b][1], h2mul(e[a][3], e[b][3]));
-                            outw[2] = h2fma(e[a][2], e[b][0], h2mul(nra01, e[b][2]));
-                            outw[3] = h2fma(e[a][3], e[b][1], h2mul(nra23, e[b][3]));
-                        } else {
-                            outw[0] = outw[1] = outw[2] = outw[3] = 0u;
-                        }
-                    } else {
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int pp = 2 * u + h;
-                            if (pp < kPairs) {
-                                const int a = PT.i[pp], b = PT.j[pp];
-                                const uint32_t nra = e[a][0] ^ 0x80008000u;
-                                outw[2 * h + 0] = h2fma(e[a][0], e[b][0], h2mul(e[a][1], e[b][1]));
-                                outw[2 * h + 1] = h2fma(e[a][1], e[b][0], h2mul(nra, e[b][1]));
-                            } else {
-                                outw[2 * h + 0] = outw[2 * h + 1] = 0u;
-                            }
-                        }
-                    }
-                    const uint32_t dst = smem_u32(sB + stage * B2_BYTES) + row_off + ((((uint32_t)u & 7u) ^ xr) << 4);
-                    st_shared_v4(dst, outw[0], outw[1], outw[2], outw[3]);
-                    if ((u & 7) == 7) {
-                        fence_proxy_async_smem();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive_cluster(&full[stage], 0);   // the leader's barrier
-                        if (++stage == STAGES2) {
-                            stage = 0;
-                            phase ^= 1;
-                        }
-                    }
-                }
-            }
+            produce_x_pair<Mi, BPC, STAGES2, B2_BYTES>(p, w, f, valid, sB, full, empty, stage, phase, row_off, xr);
         }
     }
 
