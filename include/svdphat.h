@@ -73,6 +73,8 @@ typedef struct {
     int64_t bytes_R;           /* device bytes of the split-FP16 normalised dictionary rows (SVD)               */
     int64_t bytes_workspace;   /* per-call workspace (phasors, keys, Z, ...)                                    */
     double setup_seconds;      /* wall time of svdphat_plan_create                                              */
+    int32_t srp_rows;          /* rows of the SRP GEMM: Q_classes, or the antipodal fold rows when the grid is
+                                  centrally symmetric in tau (class pairs tau_c' = -tau_c; R22)        */
 } svdphat_plan_info_t;
 
 /* Alg. 1 offline steps 1-3: TDOAs (eq. 1/2), W (eqs. 4, 8), SVD (eq. 10) with the rank rule

@@ -145,7 +145,7 @@ struct svdphat_plan_s {
         if (p.ev_join2) cudaEventDestroy(p.ev_join2);
         void* bufs[] = {p.d_W16,   p.d_V16,   p.d_R16,   p.d_rep,   p.d_delay,     p.d_window,      p.d_twN,
                         p.d_P16,   p.d_keys,  p.d_Z32,   p.d_Zs16,  p.d_zflag,     p.d_stage,       p.d_doa_stage,
-                        p.d_score_stage, p.d_S, p.d_cls, p.d_dirs, p.d_Ypart};
+                        p.d_score_stage, p.d_S, p.d_cls, p.d_dirs, p.d_Ypart, p.d_fold_cls};
         for (void* b : bufs)
             if (b) cudaFree(b);
     }
@@ -283,6 +283,56 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
         p.pair_srp = e ? atoi(e) != 0 : true;
     }
     p.Q_pad = p.pair_srp ? (p.Q_eff + 255) / 256 * 256 : (p.Q_eff + 127) / 128 * 128;
+
+    // ---- antipodal folding of the SRP GEMM (R22): class c' is the antipode of class c when its tau row is
+    // the bitwise negation of c's (far field on a centrally symmetric grid: eq. 2 is odd in s_q, so every product
+    // and sum negates exactly).  Then W_c' = conj W_c (eq. 4) and one fold row gives both scores.
+    std::vector<int> fold_m, fold_p;
+    {
+        const char* e = getenv("SVDPHAT_FOLD");
+        const bool want = (e ? atoi(e) != 0 : true) && p.pair_srp && (p.methods & SVDPHAT_METHOD_SRP);
+        if (want) {
+            auto row_hash = [&](const double* t) {
+                const unsigned char* b = reinterpret_cast<const unsigned char*>(t);
+                uint64_t hsh = 1469598103934665603ull;
+                for (size_t i = 0; i < (size_t)P * 8; ++i) hsh = (hsh ^ b[i]) * 1099511628211ull;
+                return hsh;
+            };
+            std::unordered_map<uint64_t, std::vector<int>> by_hash;
+            for (int c = 0; c < p.Q_eff; ++c) by_hash[row_hash(&tau[(size_t)p.rep_q[c] * P])].push_back(c);
+            std::vector<double> neg(P);
+            std::vector<char> used(p.Q_eff, 0);
+            for (int c = 0; c < p.Q_eff; ++c) {
+                if (used[c]) continue;
+                const double* t = &tau[(size_t)p.rep_q[c] * P];
+                for (int i = 0; i < P; ++i) neg[i] = -t[i] + 0.0;              // +0.0: rows never hold -0
+                int partner = -1;
+                auto it = by_hash.find(row_hash(neg.data()));
+                if (it != by_hash.end())
+                    for (int c2 : it->second)
+                        if (c2 != c && !used[c2] &&
+                            std::memcmp(&tau[(size_t)p.rep_q[c2] * P], neg.data(), (size_t)P * 8) == 0) {
+                            partner = c2;
+                            break;
+                        }
+                used[c] = 1;
+                if (partner >= 0) used[partner] = 1;
+                fold_m.push_back(c);
+                fold_p.push_back(partner);
+            }
+            // fold only when it removes at least a quarter of the rows
+            p.fold = 4 * (int64_t)fold_m.size() <= 3 * (int64_t)p.Q_eff;
+        }
+    }
+    if (p.fold) {
+        p.fold_rows = (int)fold_m.size();
+        p.W_rows = (p.fold_rows + 255) / 256 * 256;
+        p.spc_W = 2 * ((p.L.U + 15) / 16);
+    } else {
+        p.W_rows = (p.Q_eff + 255) / 256 * 256;
+        p.spc_W = p.L.U / 8;
+    }
+    p.K_W = (int64_t)p.L.n_chunks * p.spc_W * 64;
     {
         const char* e = getenv("SVDPHAT_PAIR_PROJ");
         p.pair_proj = e ? atoi(e) != 0 : true;
@@ -296,6 +346,12 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     SVD_CUDA_TRY(cudaMalloc(&d_tau, tau_cls.size() * 8));
     std::unique_ptr<double, decltype(&cudaFree)> tau_guard(d_tau, &cudaFree);
     SVD_CUDA_TRY(cudaMemcpy(d_tau, tau_cls.data(), tau_cls.size() * 8, cudaMemcpyHostToDevice));
+    if (p.fold) {
+        std::vector<int> fc(fold_m);
+        fc.insert(fc.end(), fold_p.begin(), fold_p.end());
+        SVD_CUDA_TRY(cudaMalloc(&p.d_fold_cls, fc.size() * sizeof(int)));
+        SVD_CUDA_TRY(cudaMemcpy(p.d_fold_cls, fc.data(), fc.size() * sizeof(int), cudaMemcpyHostToDevice));
+    }
     SVD_CUDA_TRY(cudaMalloc(&p.d_rep, (size_t)p.Q_eff * sizeof(int)));
     SVD_CUDA_TRY(cudaMemcpy(p.d_rep, p.rep_q.data(), (size_t)p.Q_eff * sizeof(int), cudaMemcpyHostToDevice));
     {
@@ -345,7 +401,7 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     if (p.methods & SVDPHAT_METHOD_SRP) {
         st = setup_srp_operand(p, d_tau);
         if (st != SVDPHAT_OK) return st;
-        if (!encode_2d(&p.tm_W, p.d_W16, p.Q_pad, p.L.K_total, 128))
+        if (!encode_2d(&p.tm_W, p.d_W16, p.W_rows, p.K_W, 128))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(W) failed");
     }
     if (p.methods & SVDPHAT_METHOD_SVD) {
@@ -380,7 +436,7 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     }
     // small batches (fewer SRP tile units than half the CTA pairs): split-K partial power maps, <= 64 MB
     if ((p.methods & SVDPHAT_METHOD_SRP) && p.pair_srp) {
-        const int64_t units = (int64_t)(p.Q_pad / 256) * ((p.max_frames + 255) / 256);
+        const int64_t units = (int64_t)(p.W_rows / 256) * ((p.max_frames + 255) / 256);
         if (units * 2 <= p.num_sms / 2) {
             const int64_t ybytes = Fp * (int64_t)p.Q_pad * (int64_t)sizeof(float);
             p.srp_split_max = (int)std::min<int64_t>(8, std::max<int64_t>(1, (64ll << 20) / ybytes));
@@ -432,6 +488,7 @@ svdphat_status svdphat_plan_info(svdphat_plan_t plan, svdphat_plan_info_t* out) 
     out->bytes_R = p.bytes_R;
     out->bytes_workspace = p.bytes_ws;
     out->setup_seconds = p.setup_seconds;
+    out->srp_rows = (p.methods & SVDPHAT_METHOD_SRP) ? (p.fold ? p.fold_rows : p.Q_eff) : 0;
     return SVDPHAT_OK;
 }
 

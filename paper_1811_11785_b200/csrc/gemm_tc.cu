@@ -45,6 +45,8 @@ struct GemmParams {
     int prefetch;                          // 0 none, 1 L2 prefetch of the next chunk's phasors, 2 same evict_last
     int bn;                                // frames per tile of the CTA-pair kernel (multiple of 32, <= 256)
     int c_lo, c_hi;                        // active bin-chunk range (band limit, NEXT-3); producer modes only
+    const int* fold_cls;                   // folded SRP (FOLD kernels): [2][fold_rows] classes of a - b / a + b
+    int fold_rows;
     int dbg;                               // timing experiments only (SVDPHAT_GEMM_DBG): 1 producer writes zeros,
                                            // 2 TMA re-loads one W tile (results invalid)
 };
@@ -385,10 +387,13 @@ constexpr int SMEM2_BYTES = 1024 + STAGES2 * (A2_BYTES + B2_BYTES) + 256;
 // XB bytes, 8 units = one 64-element slab per stage).  The frame's phasors of the current chunk stay in registers.
 // (Register double-buffering of the next chunk was tried and removed: the apparent 'load cost' was power - zeroed
 // operands keep the clock high under the cap.)
-template <int Mi, int BPC, int NSTAGES, int XB>
+// FOLD (antipodal folding, internal.h): unit u's Re words go to the Re slab and its Im words to the Im slab of slab
+// pair u/16 (8-byte stores at 8*(u%16) inside the swizzled row); the two stages of a slab pair fill together.
+template <int Mi, int BPC, int NSTAGES, int XB, bool FOLD = false>
 __device__ __forceinline__ void produce_x_pair(const GemmParams& p, const Unit& w, int f, bool valid, uint8_t* sX,
                                                uint64_t* full, uint64_t* empty, int& stage, uint32_t& phase,
                                                uint32_t row_off, uint32_t xr) {
+    static_assert(!FOLD || NSTAGES % 2 == 0, "slab pairs need an even ring");
     constexpr PairTab<Mi> PT{};
     constexpr int kPairs = Mi * (Mi - 1) / 2;
     constexpr int kUnitsRaw = (BPC == 4) ? kPairs : (kPairs + 1) / 2;
@@ -418,7 +423,14 @@ __device__ __forceinline__ void produce_x_pair(const GemmParams& p, const Unit& 
         uint32_t outw[4];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
-            if ((u & 7) == 0) mbar_wait(&empty[stage], phase ^ 1);
+            if constexpr (FOLD) {
+                if ((u & 15) == 0) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_wait(&empty[stage + 1], phase ^ 1);
+                }
+            } else {
+                if ((u & 7) == 0) mbar_wait(&empty[stage], phase ^ 1);
+            }
             if constexpr (BPC == 4) {
                 if (u < kPairs) {
                     const int a = PT.i[u], b = PT.j[u];
@@ -444,25 +456,55 @@ __device__ __forceinline__ void produce_x_pair(const GemmParams& p, const Unit& 
                     }
                 }
             }
-            const uint32_t dst = smem_u32(sX + stage * XB) + row_off + ((((uint32_t)u & 7u) ^ xr) << 4);
-            st_shared_v4(dst, outw[0], outw[1], outw[2], outw[3]);
-            if ((u & 7) == 7) {
-                fence_proxy_async_smem();
-                __syncwarp();
-                if (lane == 0) mbar_arrive_cluster(&full[stage], 0);   // the leader's barrier
-                if (++stage == NSTAGES) {
-                    stage = 0;
-                    phase ^= 1;
+            if constexpr (FOLD) {
+                // Re words: BPC 4 {Re k0k1, Re k2k3} = outw[0..1]; BPC 2 {Re p0, Re p1} = outw[0], outw[2]
+                const uint32_t re0 = outw[0], re1 = (BPC == 4) ? outw[1] : outw[2];
+                const uint32_t im0 = (BPC == 4) ? outw[2] : outw[1], im1 = outw[3];
+                const uint32_t pos = row_off + (((((uint32_t)u & 15u) >> 1) ^ xr) << 4) + (((uint32_t)u & 1u) << 3);
+                st_shared_v2(smem_u32(sX + stage * XB) + pos, re0, re1);
+                st_shared_v2(smem_u32(sX + (stage + 1) * XB) + pos, im0, im1);
+                if ((u & 15) == 15 || u == kU - 1) {
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        mbar_arrive_cluster(&full[stage], 0);
+                        mbar_arrive_cluster(&full[stage + 1], 0);
+                    }
+                    stage += 2;
+                    if (stage == NSTAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            } else {
+                const uint32_t dst = smem_u32(sX + stage * XB) + row_off + ((((uint32_t)u & 7u) ^ xr) << 4);
+                st_shared_v4(dst, outw[0], outw[1], outw[2], outw[3]);
+                if ((u & 7) == 7) {
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive_cluster(&full[stage], 0);   // the leader's barrier
+                    if (++stage == NSTAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
                 }
             }
         }
     }
 }
 
-template <int Mi, int BPC, int MODE>
+// FOLD (SRP with antipodal folding): A = fold rows, slabs alternate Re (accumulator a, TMEM columns [0,256)) and Im
+// (accumulator b, [256,512)); the epilogue scores a - b for class fold_cls[row] and a + b for fold_cls[R + row].
+// Both accumulators are live for the whole tile, so the epilogue of tile t is not overlapped with tile t+1 (~2 us
+// per ~0.5 ms tile at cfg3).
+template <int Mi, int BPC, int MODE, bool FOLD = false>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
     constexpr bool kProducer = (MODE != 2);
+    static_assert(!FOLD || kProducer, "folding applies to the producer (SRP) modes");
+    constexpr int kUnitsRaw = (BPC == 4) ? Mi * (Mi - 1) / 2 : (Mi * (Mi - 1) / 2 + 1) / 2;
+    constexpr int kU = (kUnitsRaw + 7) / 8 * 8;
+    constexpr bool kHalfPair = FOLD && (kU % 16 == 8);      // last slab pair of a chunk holds 8 units: 2 MMAs
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -536,17 +578,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                 const Unit w = unit_of(p, t);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                const uint32_t d_tmem = tmem_base + acc * BN;
                 for (int ks = w.k0; ks < w.k1; ++ks) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     if (lane == 0) {
                         const uint32_t a0 = smem_u32(sA + stage * A2_BYTES);
                         const uint32_t b0 = smem_u32(sB + stage * B2_BYTES);
+                        if constexpr (FOLD) {
+                            const int local = (ks - w.k0) % p.spc;          // slab within the bin chunk
+                            const uint32_t d_tmem = tmem_base + (uint32_t)(local & 1) * BN;   // Re -> a, Im -> b
+                            const int steps = (kHalfPair && local >= p.spc - 2) ? 2 : BK / 16;
 #pragma unroll
-                        for (int kk = 0; kk < BK / 16; ++kk)
-                            umma_f16_2sm(d_tmem, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), idesc,
-                                         (ks != w.k0) || (kk != 0));
+                            for (int kk = 0; kk < BK / 16; ++kk)
+                                if (kk < steps)
+                                    umma_f16_2sm(d_tmem, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32),
+                                                 idesc, (ks >= w.k0 + 2) || (kk != 0));
+                        } else {
+                            const uint32_t d_tmem = tmem_base + acc * BN;
+#pragma unroll
+                            for (int kk = 0; kk < BK / 16; ++kk)
+                                umma_f16_2sm(d_tmem, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32),
+                                             idesc, (ks != w.k0) || (kk != 0));
+                        }
                         umma_commit_2sm(&empty[stage], 0x3);
                     }
                     __syncwarp();
@@ -557,7 +610,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                 }
                 if (lane == 0) umma_commit_2sm(&tfull[acc], 0x3);
                 __syncwarp();
-                if (++acc == 2) {
+                if (FOLD) {
+                    acc_phase ^= 1;                                     // one accumulator pair, reused per tile
+                } else if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
                 }
@@ -574,24 +629,45 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
             tc_fence_after();
             const int row = w.m * 256 + (int)rank * 128 + g * 32 + lane;
             const bool row_ok = row < p.rows_valid;
+            int cls_m = row, cls_p = -1;                            // classes scored by this accumulator row
+            if (FOLD && row_ok) {
+                cls_m = p.fold_cls[row];
+                cls_p = p.fold_cls[p.fold_rows + row];
+            }
 #pragma unroll 1
             for (int j0 = 0; j0 < bn; j0 += 32) {
-                uint32_t r[32];
+                uint32_t r[32], rb[32];
                 tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + acc * BN + j0, r);
+                if (FOLD) tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + BN + j0, rb);
                 tmem_ld_wait();
                 const int f0 = w.n * bn + j0;
                 if (MODE == 1) {
                     if (row_ok) {
 #pragma unroll
-                        for (int jj = 0; jj < 32; ++jj)
-                            if (f0 + jj < p.F) Zs[(int64_t)(f0 + jj) * p.ldz + row] = __uint_as_float(r[jj]);
+                        for (int jj = 0; jj < 32; ++jj) {
+                            if (f0 + jj >= p.F) continue;
+                            float* zf = Zs + (int64_t)(f0 + jj) * p.ldz;
+                            if (FOLD) {
+                                const float a = __uint_as_float(r[jj]), b = __uint_as_float(rb[jj]);
+                                zf[cls_m] = a - b;
+                                if (cls_p >= 0) zf[cls_p] = a + b;
+                            } else {
+                                zf[row] = __uint_as_float(r[jj]);
+                            }
+                        }
                     }
                 } else {
                     unsigned long long k[32];
 #pragma unroll
                     for (int jj = 0; jj < 32; ++jj) {
-                        const float v = __uint_as_float(r[jj]);
-                        k[jj] = row_ok ? make_key(v, (uint32_t)row) : 0ull;
+                        if (FOLD) {
+                            const float a = __uint_as_float(r[jj]), b = __uint_as_float(rb[jj]);
+                            const unsigned long long km = row_ok ? make_key(a - b, (uint32_t)cls_m) : 0ull;
+                            const unsigned long long kp = cls_p >= 0 ? make_key(a + b, (uint32_t)cls_p) : 0ull;
+                            k[jj] = km > kp ? km : kp;
+                        } else {
+                            k[jj] = row_ok ? make_key(__uint_as_float(r[jj]), (uint32_t)row) : 0ull;
+                        }
                     }
                     const unsigned long long best = transpose_max32(k, lane);
                     if (f0 + lane < p.F && best != 0ull) atomicMax(&p.keys[f0 + lane], best);
@@ -600,7 +676,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
-            if (++acc == 2) {
+            if (FOLD) {
+                acc_phase ^= 1;
+            } else if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
             }
@@ -615,7 +693,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
             const Unit w = unit_of(p, t);
             const int f = w.n * bn + (int)rank * hb + tp;
             const bool valid = f < p.F && tp < hb && !(p.dbg & 1);
-            produce_x_pair<Mi, BPC, STAGES2, B2_BYTES>(p, w, f, valid, sB, full, empty, stage, phase, row_off, xr);
+            produce_x_pair<Mi, BPC, STAGES2, B2_BYTES, FOLD>(p, w, f, valid, sB, full, empty, stage, phase, row_off,
+                                                             xr);
         }
     }
 
@@ -869,24 +948,24 @@ static cudaError_t set_attr_one() {
                                 SMEM_BYTES);
 }
 
-template <int Mi, int BPC, int MODE>
-static cudaError_t set_attr_two() {
-    return cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                SMEM2_BYTES);
+template <int Mi, int BPC>
+static cudaError_t set_attr_pair() {
+    cudaError_t e = cudaSuccess;
+    const int sm = SMEM2_BYTES;
+    const auto attr = cudaFuncAttributeMaxDynamicSharedMemorySize;
+    if ((e = cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, 0, false>, attr, sm))) return e;
+    if ((e = cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, 1, false>, attr, sm))) return e;
+    if ((e = cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, 0, true>, attr, sm))) return e;
+    if ((e = cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, 1, true>, attr, sm))) return e;
+    return cudaFuncSetAttribute(gemm3_kernel<Mi, BPC>, attr, SMEM3_BYTES);
 }
 
 cudaError_t gemm_set_attributes() {
     cudaError_t e = cudaSuccess;
-    if ((e = set_attr_two<4, 4, 0>()) != cudaSuccess) return e;
-    if ((e = set_attr_two<8, 4, 0>()) != cudaSuccess) return e;
-    if ((e = set_attr_two<16, 4, 0>()) != cudaSuccess) return e;
-    if ((e = set_attr_two<32, 2, 0>()) != cudaSuccess) return e;
-    if ((e = cudaFuncSetAttribute(gemm3_kernel<4, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_BYTES))) return e;
-    if ((e = cudaFuncSetAttribute(gemm3_kernel<8, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_BYTES))) return e;
-    if ((e = cudaFuncSetAttribute(gemm3_kernel<16, 4>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_BYTES)))
-        return e;
-    if ((e = cudaFuncSetAttribute(gemm3_kernel<32, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM3_BYTES)))
-        return e;
+    if ((e = set_attr_pair<4, 4>()) != cudaSuccess) return e;
+    if ((e = set_attr_pair<8, 4>()) != cudaSuccess) return e;
+    if ((e = set_attr_pair<16, 4>()) != cudaSuccess) return e;
+    if ((e = set_attr_pair<32, 2>()) != cudaSuccess) return e;
 #define SVD_ATTR(MI, B)                                        \
     if ((e = set_attr_one<MI, B, 0>()) != cudaSuccess) return e; \
     if ((e = set_attr_one<MI, B, 1>()) != cudaSuccess) return e;
@@ -896,11 +975,27 @@ cudaError_t gemm_set_attributes() {
     SVD_ATTR(32, 2)
 #undef SVD_ATTR
     if ((e = set_attr_one<4, 4, 3>()) != cudaSuccess) return e;
-    if ((e = set_attr_two<4, 4, 1>()) != cudaSuccess) return e;
-    if ((e = set_attr_two<8, 4, 1>()) != cudaSuccess) return e;
-    if ((e = set_attr_two<16, 4, 1>()) != cudaSuccess) return e;
-    if ((e = set_attr_two<32, 2, 1>()) != cudaSuccess) return e;
     return set_attr_one<4, 4, 2>();
+}
+
+// CTA-pair launch over the instantiated mic counts; MODE 0 argmax / 1 store, FOLD = antipodally folded W
+template <int MODE>
+static cudaError_t launch_pair(const Plan& p, const CUtensorMap& A, const CUtensorMap& B, const GemmParams& gp,
+                               int pairs, bool fold, cudaStream_t s) {
+#define SVD_PAIR(MI, BP)                                                                                  \
+    if (p.L.Mi == MI) {                                                                                  \
+        if (fold)                                                                                        \
+            gemm2_kernel<MI, BP, MODE, true><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(A, B, gp);        \
+        else                                                                                             \
+            gemm2_kernel<MI, BP, MODE, false><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(A, B, gp);       \
+        return cudaGetLastError();                                                                       \
+    }
+    SVD_PAIR(4, 4)
+    SVD_PAIR(8, 4)
+    SVD_PAIR(16, 4)
+    SVD_PAIR(32, 2)
+#undef SVD_PAIR
+    return cudaErrorInvalidValue;
 }
 
 template <int Mi, int BPC, int MODE>
@@ -944,7 +1039,8 @@ void set_band(Plan& p, int k_lo, int k_hi, const uint8_t* mask, int64_t mask_str
 
 cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
     GemmParams gp{};
-    const bool producer_mode = (mode == 0 || mode == 1 || mode == 3);
+    const bool srp_mode = (mode == 0 || mode == 3);             // W16 operand (folded when p.fold)
+    const bool producer_mode = srp_mode || mode == 1;
     gp.c_lo = producer_mode ? p.c_lo : 0;
     gp.c_hi = producer_mode ? p.c_hi : 0;
     gp.P16 = p.d_P16;
@@ -956,15 +1052,17 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
     gp.Z = p.d_Z32;
     gp.ldz = 2 * p.Dh;
     gp.ksplit = 1;
-    gp.spc = p.L.U / 8;
+    gp.spc = srp_mode ? p.spc_W : p.L.U / 8;
     gp.bn = BN;
+    gp.fold_cls = p.d_fold_cls;
+    gp.fold_rows = p.fold_rows;
     static const int dbg = [] {
         const char* e = getenv("SVDPHAT_GEMM_DBG");
         return e ? atoi(e) : 0;
     }();
     gp.dbg = dbg;
-    static const int fixed_bn = [] {
-        const char* e = getenv("SVDPHAT_PAIR_BN");
+    static const int fixed_bn = [] {   // frames per SRP pair tile (multiple of 32, 128..256); r01: 224 (the wave-
+        const char* e = getenv("SVDPHAT_PAIR_BN");   // quantisation optimum) ran slower under the power cap than 256
         return e ? atoi(e) : 0;
     }();
     static const int pf = [] {
@@ -974,54 +1072,37 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
     gp.prefetch = pf;
     const CUtensorMap* A = nullptr;
     const CUtensorMap* B = &p.tm_W;  // unused placeholder for producer modes
-    if (mode == 0) {
+    const int npairs = p.num_sms / 2;
+    if (srp_mode) {
         A = &p.tm_W;
-        gp.n_slabs = (int)(p.L.K_total / BK);
-        gp.m_tiles = p.Q_pad / BM;
-        gp.rows_valid = p.Q_eff;
+        gp.n_slabs = (int)(p.K_W / BK);
+        gp.rows_valid = p.fold ? p.fold_rows : p.Q_eff;
+        gp.m_tiles = p.W_rows / (p.pair_srp ? 256 : BM);
     } else if (mode == 1) {
         A = &p.tm_V;
         gp.n_slabs = (int)(p.L.K_total / BK);
         gp.m_tiles = (2 * p.Dh) / BM;
         gp.rows_valid = 2 * p.Dh;
-    } else if (mode == 2) {
-        A = &p.tm_R;
-        B = &p.tm_Zs;
-        gp.keys = p.d_keys + p.F_pad;
-        gp.n_slabs = p.K2 / BK;
-        gp.m_tiles = p.Q_pad / BM;
-        gp.rows_valid = p.Q_eff;
-    } else if (mode == 3) {            // SRP power map Y[f][class] -> S (multi-source search)
-        A = &p.tm_W;
-        gp.n_slabs = (int)(p.L.K_total / BK);
-        gp.rows_valid = p.Q_eff;
-        gp.Z = p.d_S;
-        gp.ldz = p.Q_pad;
-    } else {                           // mode 4: SVD search power map Re{Dhat Zhat}[f][class] -> S
+    } else {                           // 2: SVD search + argmax; 4: its power map Re{Dhat Zhat}[f][class] -> S
         A = &p.tm_R;
         B = &p.tm_Zs;
         gp.n_slabs = p.K2 / BK;
         gp.m_tiles = p.Q_pad / BM;
         gp.rows_valid = p.Q_eff;
-        gp.Z = p.d_S;
-        gp.ldz = p.Q_pad;
+        if (mode == 2) {
+            gp.keys = p.d_keys + p.F_pad;
+        } else {
+            gp.Z = p.d_S;
+            gp.ldz = p.Q_pad;
+        }
     }
-    if (mode == 3) {
-        gp.m_tiles = p.Q_pad / 256;
+    if (mode == 3) {                   // SRP power map Y[f][class] -> S (multi-source search); pair kernel, store
+        gp.m_tiles = p.W_rows / 256;
+        gp.Z = p.d_S;
+        gp.ldz = p.Q_pad;
         const int units = gp.m_tiles * gp.n_tiles;
-        const int pairs = units < p.num_sms / 2 ? units : p.num_sms / 2;
         if (units == 0) return cudaSuccess;
-#define SVD_DISPATCH4(MI, BP)                                                                  \
-    if (p.L.Mi == MI) {                                                                       \
-        gemm2_kernel<MI, BP, 1><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(*A, *B, gp);          \
-        return cudaGetLastError();                                                            \
-    }
-        SVD_DISPATCH4(4, 4)
-        SVD_DISPATCH4(8, 4)
-        SVD_DISPATCH4(16, 4)
-        SVD_DISPATCH4(32, 2)
-#undef SVD_DISPATCH4
-        return cudaErrorInvalidValue;
+        return launch_pair<1>(p, *A, *B, gp, units < npairs ? units : npairs, p.fold, s);
     }
     int tiles = gp.m_tiles * gp.n_tiles;
     if (mode == 1) {
@@ -1031,19 +1112,8 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
         if (sh.pair) {
             gp.m_tiles = sh.m_tiles;
             const int units = gp.m_tiles * gp.n_tiles * gp.ksplit;
-            const int pairs = units < p.num_sms / 2 ? units : p.num_sms / 2;
             if (units == 0) return cudaSuccess;
-#define SVD_DISPATCH6(MI, BP)                                                                 \
-    if (p.L.Mi == MI) {                                                                      \
-        gemm2_kernel<MI, BP, 1><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(*A, *B, gp);         \
-        return cudaGetLastError();                                                           \
-    }
-            SVD_DISPATCH6(4, 4)
-            SVD_DISPATCH6(8, 4)
-            SVD_DISPATCH6(16, 4)
-            SVD_DISPATCH6(32, 2)
-#undef SVD_DISPATCH6
-            return cudaErrorInvalidValue;
+            return launch_pair<1>(p, *A, *B, gp, units < npairs ? units : npairs, false, s);
         }
         tiles *= gp.ksplit;
     }
@@ -1055,11 +1125,10 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
         const char* e = getenv("SVDPHAT_SRP_TS");   // TS variant: correct, but 3% slower at cfg3 (r01 ncu:
         return e ? atoi(e) : 0;                    // tensor pipe 74% active although the MMA never waits)
     }();
-    if (mode == 0 && p.pair_srp && ts) {
-        gp.m_tiles = p.Q_pad / 256;
+    if (mode == 0 && p.pair_srp && ts && !p.fold) {
         gp.n_tiles = (F + 255) / 256;
         const int units = gp.m_tiles * gp.n_tiles;
-        const int pairs = units < p.num_sms / 2 ? units : p.num_sms / 2;
+        const int pairs = units < npairs ? units : npairs;
 #define SVD_DISPATCH3(MI, BP)                                                          \
     if (p.L.Mi == MI) {                                                               \
         gemm3_kernel<MI, BP><<<2 * pairs, THREADS3, SMEM3_BYTES, s>>>(*A, gp);        \
@@ -1074,59 +1143,23 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
     }
     if (mode == 0 && p.pair_srp && p.srp_split_max > 1) {
         // small batch: fewer units than half the CTA pairs -> split K into chunk ranges with partial power maps
-        const int m2 = p.Q_pad / 256, units = m2 * gp.n_tiles, npairs = p.num_sms / 2;
+        const int units = gp.m_tiles * gp.n_tiles;
         int S = units > 0 ? npairs / units : 1;
         S = S < p.srp_split_max ? S : p.srp_split_max;
         S = S < p.c_hi - p.c_lo ? S : p.c_hi - p.c_lo;
         if (units * 2 <= npairs && S > 1) {
-            gp.m_tiles = m2;
             gp.ksplit = S;
             gp.Z = p.d_Ypart;
             gp.ldz = p.Q_pad;
-            const int pairs = units * S < npairs ? units * S : npairs;
-#define SVD_DISPATCH5(MI, BP)                                                                 \
-    if (p.L.Mi == MI) {                                                                      \
-        gemm2_kernel<MI, BP, 1><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(*A, *B, gp);         \
-        cudaError_t e = cudaGetLastError();                                                  \
-        return e != cudaSuccess ? e : launch_split_argmax(p, F, S, s);                       \
-    }
-            SVD_DISPATCH5(4, 4)
-            SVD_DISPATCH5(8, 4)
-            SVD_DISPATCH5(16, 4)
-            SVD_DISPATCH5(32, 2)
-#undef SVD_DISPATCH5
-            return cudaErrorInvalidValue;
+            const cudaError_t e = launch_pair<1>(p, *A, *B, gp, units * S < npairs ? units * S : npairs, p.fold, s);
+            return e != cudaSuccess ? e : launch_split_argmax(p, F, S, s);
         }
     }
     if (mode == 0 && p.pair_srp) {
-        gp.m_tiles = p.Q_pad / 256;
-        // frames per pair tile: 256 unless SVDPHAT_PAIR_BN picks another multiple of 32 (r01 measurement: the
-        // wave-quantisation optimum 224 ran slower at cfg3 under the power cap than 256)
-        const int npairs = p.num_sms / 2;
-        long best = -1;
-        for (int bn = 256; bn >= 128; bn -= 32) {
-            if (bn != (fixed_bn ? fixed_bn : 256)) continue;
-            const long nt = (F + bn - 1) / bn;
-            const long waves = (gp.m_tiles * nt + npairs - 1) / npairs;
-            if (best < 0 || waves * bn < best) {
-                best = waves * bn;
-                gp.bn = bn;
-                gp.n_tiles = (int)nt;
-            }
-        }
+        gp.bn = fixed_bn ? fixed_bn : 256;
+        gp.n_tiles = (F + gp.bn - 1) / gp.bn;
         const int units = gp.m_tiles * gp.n_tiles;
-        const int pairs = units < npairs ? units : npairs;
-#define SVD_DISPATCH2(MI, BP)                                                                                \
-    if (p.L.Mi == MI) {                                                                                     \
-        gemm2_kernel<MI, BP, 0><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(*A, *B, gp);                        \
-        return cudaGetLastError();                                                                          \
-    }
-        SVD_DISPATCH2(4, 4)
-        SVD_DISPATCH2(8, 4)
-        SVD_DISPATCH2(16, 4)
-        SVD_DISPATCH2(32, 2)
-#undef SVD_DISPATCH2
-        return cudaErrorInvalidValue;
+        return launch_pair<0>(p, *A, *B, gp, units < npairs ? units : npairs, p.fold, s);
     }
 #define SVD_DISPATCH(MI, BP)                                                                      \
     if (p.L.Mi == MI) {                                                                          \

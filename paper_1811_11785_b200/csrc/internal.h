@@ -46,7 +46,17 @@ struct Plan {
     std::vector<double> sigma2;   // descending
     double setup_seconds = 0;
     // device operands (owned)
-    __half* d_W16 = nullptr;      // [Q_pad][K_total]
+    __half* d_W16 = nullptr;      // [W_rows][K_W]: class rows (standard kappa) or fold rows (fold kappa)
+    // antipodal folding of the SRP GEMM (R22): class c' with tau_c' = -tau_c bitwise has W_c' = conj W_c,
+    // so one fold row carrying (Re W_c, Im W_c) yields Y_c = a - b and Y_c' = a + b with a = Re W_c . x_r and
+    // b = Im W_c . x_i: half the rows, same K.  Fold kappa: per chunk, SP = ceil(U/16) slab pairs (Re slab, Im slab);
+    // unit u's 4 Re values sit at 4*(u%16) of Re slab u/16, its 4 Im values likewise in the Im slab.
+    bool fold = false;
+    int fold_rows = 0;            // rows of the folded W (classes paired with their antipode, or alone)
+    int* d_fold_cls = nullptr;    // [2][fold_rows]: class of a - b, class of a + b (-1: none)
+    int W_rows = 0;               // rows of W16 (multiple of 256 for the pair kernel)
+    int64_t K_W = 0;              // contraction length of W16
+    int spc_W = 0;                // W16 slabs per bin chunk
     __half* d_V16 = nullptr;      // [2*Dh][K_total]
     __half* d_R16 = nullptr;      // [Q_pad][K2]
     int* d_rep = nullptr;         // [Q_eff]

@@ -1,7 +1,8 @@
 // setup.cu — Alg. 1 offline in float64, run once per plan on the device.
 //
 //  * W16 : W_{q,i,j}[k] = exp(+j 2 pi k tau_{q,i,j} / N) (eq. 4) packed real-split FP16 as
-//          [Re W | -Im W] in the GEMM contraction order (internal.h), one row per steering class.
+//          [Re W | -Im W] in the GEMM contraction order (internal.h), one row per steering class; or folded (one
+//          row per antipodal class pair, Re and Im in separate slabs, R22).
 //  * SVD : sigma^2 and U from the Hermitian Gram G = W W^H (same singular values / left vectors as eq. 10),
 //          with G built in closed form: G_ab = sum_p sum_{k<Kb} e^{j 2 pi k (tau_ap - tau_bp)/N}
 //          = sum_p e^{j pi (Kb-1) x} sin(pi Kb x) / sin(pi x),  x = (tau_ap - tau_bp)/N  (geometric series).
@@ -55,6 +56,38 @@ __global__ void pack_w16_kernel(const double* __restrict__ tau, int Q_eff, int P
         sincospi(2.0 * (double)k * t / (double)N, &s, &c);  // e^{j 2 pi k tau / N}
         dst[kappa_of(pi, k, 0, bpc, U)] = __double2half(c);
         dst[kappa_of(pi, k, 1, bpc, U)] = __double2half(-s);
+    }
+}
+
+// Folded W (antipodal folding, internal.h / DESIGN.md R22): fold row r carries class fold_m[r]'s Re W in the Re slabs
+// and its Im W (sign +: b = Im W . x_i, Y = a - b, Y_antipode = a + b) in the Im slabs.  Unit u of chunk c, value s
+// (BPC 4: bin 4c+s; BPC 2: pair 2u + s/2, bin 2c + s%2) sits at ((c*SP + u/16)*2 + im)*64 + (u%16)*4 + s.
+__host__ __device__ __forceinline__ int64_t kappa_fold(int pi, int k, int im, int bpc, int SP) {
+    const int c = k / bpc;
+    const int u = (bpc == 4) ? pi : (pi >> 1);
+    const int s = (bpc == 4) ? (k % 4) : ((pi & 1) * 2 + k % 2);
+    return (((int64_t)c * SP + u / 16) * 2 + im) * 64 + (u % 16) * 4 + s;
+}
+
+__global__ void pack_w16f_kernel(const double* __restrict__ tau, const int* __restrict__ fold_m, int rows, int P,
+                                 int M, int Mi, int N, int Kb, int bpc, int SP, int64_t K_W,
+                                 __half* __restrict__ W16) {
+    const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid >= (int64_t)rows * P) return;
+    const int row = (int)(tid / P), p = (int)(tid % P);
+    int i = 0, rem = p;
+    while (rem >= M - 1 - i) {
+        rem -= M - 1 - i;
+        ++i;
+    }
+    const int pi = pair_index(i, i + 1 + rem, Mi);
+    const double t = tau[(int64_t)fold_m[row] * P + p];
+    __half* dst = W16 + (int64_t)row * K_W;
+    for (int k = 0; k < Kb; ++k) {
+        double sn, cs;
+        sincospi(2.0 * (double)k * t / (double)N, &sn, &cs);  // e^{j 2 pi k tau / N}
+        dst[kappa_fold(pi, k, 0, bpc, SP)] = __double2half(cs);
+        dst[kappa_fold(pi, k, 1, bpc, SP)] = __double2half(sn);
     }
 }
 
@@ -176,12 +209,18 @@ __global__ void pack_r16_kernel(const cuDoubleComplex* __restrict__ Uv, const do
 static inline unsigned cdiv(int64_t a, int64_t b) { return (unsigned)((a + b - 1) / b); }
 
 svdphat_status setup_srp_operand(Plan& p, const double* d_tau_cls) {
-    p.bytes_W = (int64_t)p.Q_pad * p.L.K_total * 2;
+    p.bytes_W = (int64_t)p.W_rows * p.K_W * 2;
     SVD_CUDA_TRY(cudaMalloc(&p.d_W16, p.bytes_W));
     SVD_CUDA_TRY(cudaMemset(p.d_W16, 0, p.bytes_W));
-    const int64_t n = (int64_t)p.Q_eff * p.P;
-    pack_w16_kernel<<<cdiv(n, 256), 256>>>(d_tau_cls, p.Q_eff, p.P, p.M, p.L.Mi, p.N, p.Kb, p.L.bpc, p.L.U,
-                                           p.L.K_total, p.d_W16);
+    if (p.fold) {
+        const int64_t n = (int64_t)p.fold_rows * p.P;
+        pack_w16f_kernel<<<cdiv(n, 256), 256>>>(d_tau_cls, p.d_fold_cls, p.fold_rows, p.P, p.M, p.L.Mi, p.N, p.Kb,
+                                                p.L.bpc, p.spc_W / 2, p.K_W, p.d_W16);
+    } else {
+        const int64_t n = (int64_t)p.Q_eff * p.P;
+        pack_w16_kernel<<<cdiv(n, 256), 256>>>(d_tau_cls, p.Q_eff, p.P, p.M, p.L.Mi, p.N, p.Kb, p.L.bpc, p.L.U,
+                                               p.K_W, p.d_W16);
+    }
     SVD_CUDA_TRY(cudaGetLastError());
     SVD_CUDA_TRY(cudaDeviceSynchronize());
     return SVDPHAT_OK;

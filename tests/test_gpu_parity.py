@@ -596,3 +596,55 @@ def test_odd_strides_same_results():
     torch.cuda.synchronize()
     assert torch.equal(d1, d2) and torch.equal(s1, s2)
     plan.close()
+
+
+@pytest.mark.parametrize("M", [3, 7, 12, 20])
+def test_antipodal_fold(M, monkeypatch):
+    """DESIGN.md R22: on a far-field grid closed under s -> -s, the SRP GEMM runs on fold rows (a class and its
+    antipode share one row; Y_c = a - b, Y_c' = a + b) — half the rows — and every instantiated mic count (record
+    layouts with and without a half slab pair) gives the oracle's SRP-PHAT result, the same DOAs as the unfolded
+    GEMM (SVDPHAT_FOLD=0), and the same multi-source peaks (the fold's power-map store).  A grid without central
+    symmetry is not folded."""
+    from workloads import geometry as G
+    from workloads import scenes as SC
+    rng = np.random.default_rng(4242 + M)
+    mics = rng.uniform(-0.07, 0.07, (M, 3))
+    pts = G.icosphere(3)
+    N, hop, F = 256, 128, 300
+    L = (F - 1) * hop + N
+    u = pts[rng.integers(len(pts))]
+    audio = SC.plane_wave_stream(rng, mics, 16000.0, 343.0, L, u, 10.0).astype(np.float32)
+    d_audio = torch.from_numpy(audio).to(DEV)
+    res = {}
+    for fold in ("1", "0"):
+        monkeypatch.setenv("SVDPHAT_FOLD", fold)
+        plan = S.Plan(mics, pts, 16000.0, 343.0, N, hop, "far", methods=("srp",), max_frames=F)
+        inf = plan.info()
+        assert inf["srp_rows"] == (inf["Q_classes"] // 2 if fold == "1" else inf["Q_classes"])
+        doa = torch.empty(F, dtype=torch.int32, device=DEV)
+        sc = torch.empty(F, dtype=torch.float32, device=DEV)
+        plan.localize("srp", d_audio, F, L, hop, doa, sc, torch.cuda.current_stream().cuda_stream)
+        dk = torch.empty(F * 2, dtype=torch.int32, device=DEV)
+        sk = torch.empty(F * 2, dtype=torch.float32, device=DEV)
+        plan.localize_topk("srp", d_audio, F, L, hop, 2, 30.0, dk, sk, torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        res[fold] = (doa.cpu().numpy(), sc.cpu().numpy(), dk.cpu().numpy(), sk.cpu().numpy())
+        plan.close()
+    tau = srp.tdoa(mics, pts, 16000.0, 343.0, "far")
+    x = srp.frames_to_x(srp.extract_frames(audio, F, M, N, L, hop))
+    P_, Y_at = PP.srp_reference(tau, x, N)
+    PP.compare(res["1"][0], res["1"][1], P_, Y_at, f"M={M} folded")
+    same = res["1"][0] == res["0"][0]
+    assert same.mean() >= 0.99
+    for f in np.nonzero(~same)[0]:             # only near-ties may differ (fp32 order: a - b vs one sum)
+        a, b = res["1"][0][f], res["0"][0][f]
+        assert abs(P_[f, a] - P_[f, b]) <= 2e-3 * abs(P_[f].max())
+    assert np.mean(res["1"][2] == res["0"][2]) >= 0.98
+    np.testing.assert_array_equal(res["1"][1][same], res["0"][1][same])     # same q -> same eq.-5 score
+    # a grid without central symmetry: no antipodes, no fold
+    monkeypatch.setenv("SVDPHAT_FOLD", "1")
+    jitter = pts + rng.normal(0.0, 1e-3, pts.shape)
+    plan = S.Plan(mics, jitter, 16000.0, 343.0, N, hop, "far", methods=("srp",), max_frames=F)
+    inf = plan.info()
+    assert inf["srp_rows"] == inf["Q_classes"]
+    plan.close()
