@@ -388,7 +388,7 @@ constexpr int SMEM2_BYTES = 1024 + STAGES2 * (A2_BYTES + B2_BYTES) + 256;
 // (Register double-buffering of the next chunk was tried and removed: the apparent 'load cost' was power - zeroed
 // operands keep the clock high under the cap.)
 // FOLD (antipodal folding, internal.h): unit u's Re words go to the Re slab and its Im words to the Im slab of slab
-// pair u/16 (8-byte stores at 8*(u%16) inside the swizzled row); the two stages of a slab pair fill together.
+// pair u/16 (at byte 8*(u%16) of the swizzled row); the two stages of a slab pair fill together.
 template <int Mi, int BPC, int NSTAGES, int XB, bool FOLD = false>
 __device__ __forceinline__ void produce_x_pair(const GemmParams& p, const Unit& w, int f, bool valid, uint8_t* sX,
                                                uint64_t* full, uint64_t* empty, int& stage, uint32_t& phase,
@@ -420,7 +420,7 @@ __device__ __forceinline__ void produce_x_pair(const GemmParams& p, const Unit& 
                 e[m][1] = v.y;
             }
         }
-        uint32_t outw[4];
+        uint32_t outw[4], pend[4];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             if constexpr (FOLD) {
@@ -457,12 +457,21 @@ __device__ __forceinline__ void produce_x_pair(const GemmParams& p, const Unit& 
                 }
             }
             if constexpr (FOLD) {
-                // Re words: BPC 4 {Re k0k1, Re k2k3} = outw[0..1]; BPC 2 {Re p0, Re p1} = outw[0], outw[2]
+                // Re words: BPC 4 {Re k0k1, Re k2k3} = outw[0..1]; BPC 2 {Re p0, Re p1} = outw[0], outw[2].
+                // Units 2j and 2j+1 share the 16-byte chunk j of a slab row: one STS.128 per slab per unit pair
+                // (two STS.64 per unit were 4-way bank-conflicted: 505M conflicts, tensor pipe 59%).
                 const uint32_t re0 = outw[0], re1 = (BPC == 4) ? outw[1] : outw[2];
                 const uint32_t im0 = (BPC == 4) ? outw[2] : outw[1], im1 = outw[3];
-                const uint32_t pos = row_off + (((((uint32_t)u & 15u) >> 1) ^ xr) << 4) + (((uint32_t)u & 1u) << 3);
-                st_shared_v2(smem_u32(sX + stage * XB) + pos, re0, re1);
-                st_shared_v2(smem_u32(sX + (stage + 1) * XB) + pos, im0, im1);
+                if ((u & 1) == 0) {
+                    pend[0] = re0;
+                    pend[1] = re1;
+                    pend[2] = im0;
+                    pend[3] = im1;
+                } else {
+                    const uint32_t pos = row_off + (((((uint32_t)u & 15u) >> 1) ^ xr) << 4);
+                    st_shared_v4(smem_u32(sX + stage * XB) + pos, pend[0], pend[1], re0, re1);
+                    st_shared_v4(smem_u32(sX + (stage + 1) * XB) + pos, pend[2], pend[3], im0, im1);
+                }
                 if ((u & 15) == 15 || u == kU - 1) {
                     fence_proxy_async_smem();
                     __syncwarp();
@@ -569,7 +578,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
             }
         }
     } else if (warp == 1) {
-        if (leader) {
+        // MMA issuer: one thread.  Descriptors advance by constant offsets (stage: bytes >> 4; K step of 16 halves:
+        // 32 B >> 4 = 2) and the fold's slab parity / half-pair test use counters, so the per-slab issue cost stays
+        // well under the 512 MMA cycles of a slab (ncu r01: an integer modulo here left the tensor pipe 40% idle).
+        if (leader && lane == 0) {
+            const uint64_t adesc0 = umma_desc_sw128(smem_u32(sA)), bdesc0 = umma_desc_sw128(smem_u32(sB));
             int stage = 0;
             uint32_t phase = 0;
             int acc = 0;
@@ -578,38 +591,37 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                 const Unit w = unit_of(p, t);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
+                int local = 0;                                      // slab index within the bin chunk (FOLD)
                 for (int ks = w.k0; ks < w.k1; ++ks) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    if (lane == 0) {
-                        const uint32_t a0 = smem_u32(sA + stage * A2_BYTES);
-                        const uint32_t b0 = smem_u32(sB + stage * B2_BYTES);
-                        if constexpr (FOLD) {
-                            const int local = (ks - w.k0) % p.spc;          // slab within the bin chunk
-                            const uint32_t d_tmem = tmem_base + (uint32_t)(local & 1) * BN;   // Re -> a, Im -> b
-                            const int steps = (kHalfPair && local >= p.spc - 2) ? 2 : BK / 16;
-#pragma unroll
-                            for (int kk = 0; kk < BK / 16; ++kk)
-                                if (kk < steps)
-                                    umma_f16_2sm(d_tmem, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32),
-                                                 idesc, (ks >= w.k0 + 2) || (kk != 0));
-                        } else {
-                            const uint32_t d_tmem = tmem_base + acc * BN;
-#pragma unroll
-                            for (int kk = 0; kk < BK / 16; ++kk)
-                                umma_f16_2sm(d_tmem, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32),
-                                             idesc, (ks != w.k0) || (kk != 0));
+                    const uint64_t ad = adesc0 + (uint64_t)(stage * (A2_BYTES >> 4));
+                    const uint64_t bd = bdesc0 + (uint64_t)(stage * (B2_BYTES >> 4));
+                    if constexpr (FOLD) {
+                        const uint32_t d_tmem = tmem_base + (uint32_t)(local & 1) * BN;   // Re -> a, Im -> b
+                        const bool half = kHalfPair && local >= p.spc - 2;
+                        const uint32_t acc0 = ks >= w.k0 + 2;
+                        umma_f16_2sm(d_tmem, ad, bd, idesc, acc0);
+                        umma_f16_2sm(d_tmem, ad + 2, bd + 2, idesc, 1u);
+                        if (!half) {
+                            umma_f16_2sm(d_tmem, ad + 4, bd + 4, idesc, 1u);
+                            umma_f16_2sm(d_tmem, ad + 6, bd + 6, idesc, 1u);
                         }
-                        umma_commit_2sm(&empty[stage], 0x3);
+                        if (++local == p.spc) local = 0;
+                    } else {
+                        const uint32_t d_tmem = tmem_base + acc * BN;
+                        const uint32_t acc0 = ks != w.k0;
+#pragma unroll
+                        for (int kk = 0; kk < BK / 16; ++kk)
+                            umma_f16_2sm(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, kk ? 1u : acc0);
                     }
-                    __syncwarp();
+                    umma_commit_2sm(&empty[stage], 0x3);
                     if (++stage == STAGES2) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                if (lane == 0) umma_commit_2sm(&tfull[acc], 0x3);
-                __syncwarp();
+                umma_commit_2sm(&tfull[acc], 0x3);
                 if (FOLD) {
                     acc_phase ^= 1;                                     // one accumulator pair, reused per tile
                 } else if (++acc == 2) {
@@ -618,6 +630,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                 }
             }
         }
+        __syncwarp();
     } else if (warp >= 2 && warp < 6) {
         const int g = warp & 3;
         int acc = 0;
