@@ -578,10 +578,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
             }
         }
     } else if (warp == 1) {
-        // MMA issuer: one thread.  Descriptors advance by constant offsets (stage: bytes >> 4; K step of 16 halves:
+        // MMA issuer: the whole warp, converged; elect.sync inside the issue asm picks one lane.  Descriptors advance by constant offsets (stage: bytes >> 4; K step of 16 halves:
         // 32 B >> 4 = 2) and the fold's slab parity / half-pair test use counters, so the per-slab issue cost stays
         // well under the 512 MMA cycles of a slab (ncu r01: an integer modulo here left the tensor pipe 40% idle).
-        if (leader && lane == 0) {
+        if (leader) {
             const uint64_t adesc0 = umma_desc_sw128(smem_u32(sA)), bdesc0 = umma_desc_sw128(smem_u32(sB));
             int stage = 0;
             uint32_t phase = 0;
@@ -601,11 +601,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                         const uint32_t d_tmem = tmem_base + (uint32_t)(local & 1) * BN;   // Re -> a, Im -> b
                         const bool half = kHalfPair && local >= p.spc - 2;
                         const uint32_t acc0 = ks >= w.k0 + 2;
-                        umma_f16_2sm(d_tmem, ad, bd, idesc, acc0);
-                        umma_f16_2sm(d_tmem, ad + 2, bd + 2, idesc, 1u);
+                        umma_f16_2sm_warp(d_tmem, ad, bd, idesc, acc0);
+                        umma_f16_2sm_warp(d_tmem, ad + 2, bd + 2, idesc, 1u);
                         if (!half) {
-                            umma_f16_2sm(d_tmem, ad + 4, bd + 4, idesc, 1u);
-                            umma_f16_2sm(d_tmem, ad + 6, bd + 6, idesc, 1u);
+                            umma_f16_2sm_warp(d_tmem, ad + 4, bd + 4, idesc, 1u);
+                            umma_f16_2sm_warp(d_tmem, ad + 6, bd + 6, idesc, 1u);
                         }
                         if (++local == p.spc) local = 0;
                     } else {
@@ -613,15 +613,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                         const uint32_t acc0 = ks != w.k0;
 #pragma unroll
                         for (int kk = 0; kk < BK / 16; ++kk)
-                            umma_f16_2sm(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, kk ? 1u : acc0);
+                            umma_f16_2sm_warp(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, kk ? 1u : acc0);
                     }
-                    umma_commit_2sm(&empty[stage], 0x3);
+                    umma_commit_2sm_warp(&empty[stage], 0x3);
                     if (++stage == STAGES2) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
-                umma_commit_2sm(&tfull[acc], 0x3);
+                umma_commit_2sm_warp(&tfull[acc], 0x3);
                 if (FOLD) {
                     acc_phase ^= 1;                                     // one accumulator pair, reused per tile
                 } else if (++acc == 2) {
@@ -630,7 +630,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                 }
             }
         }
-        __syncwarp();
     } else if (warp >= 2 && warp < 6) {
         const int g = warp & 3;
         int acc = 0;
