@@ -185,7 +185,8 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
             }
         }
     } else if (warp == 1) {
-        // ============================================================ MMA issuer
+        // ============================================================ MMA issuer (converged warp, elect.sync in the asm)
+        const uint64_t adesc0 = umma_desc_sw128(smem_u32(sA)), bdesc0 = umma_desc_sw128(smem_u32(sB));
         int stage = 0;
         uint32_t phase = 0;
         int acc = 0;
@@ -198,24 +199,19 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
             for (int ks = w.k0; ks < w.k1; ++ks) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
-                if (lane == 0) {
-                    const uint32_t a0 = smem_u32(sA + stage * A_BYTES);
-                    const uint32_t b0 = smem_u32(sB + stage * B_BYTES);
+                const uint64_t ad = adesc0 + (uint64_t)(stage * (A_BYTES >> 4));
+                const uint64_t bd = bdesc0 + (uint64_t)(stage * (B_BYTES >> 4));
+                const uint32_t acc0 = ks != w.k0;
 #pragma unroll
-                    for (int kk = 0; kk < BK / 16; ++kk) {
-                        umma_f16(d_tmem, umma_desc_sw128(a0 + kk * 32), umma_desc_sw128(b0 + kk * 32), kIdesc,
-                                 (ks != w.k0) || (kk != 0));
-                    }
-                    umma_commit(&empty[stage]);
-                }
-                __syncwarp();
+                for (int kk = 0; kk < BK / 16; ++kk)
+                    umma_f16_warp(d_tmem, ad + 2 * kk, bd + 2 * kk, kIdesc, kk ? 1u : acc0);
+                umma_commit_warp(&empty[stage]);
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
-            if (lane == 0) umma_commit(&tfull[acc]);
-            __syncwarp();
+            umma_commit_warp(&tfull[acc]);
             if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
