@@ -145,7 +145,7 @@ struct svdphat_plan_s {
         if (p.ev_join2) cudaEventDestroy(p.ev_join2);
         void* bufs[] = {p.d_W16,   p.d_V16,   p.d_R16,   p.d_rep,   p.d_delay,     p.d_window,      p.d_twN,
                         p.d_P16,   p.d_keys,  p.d_Z32,   p.d_Zs16,  p.d_zflag,     p.d_stage,       p.d_doa_stage,
-                        p.d_score_stage, p.d_S, p.d_cls, p.d_dirs, p.d_Ypart, p.d_fold_cls};
+                        p.d_score_stage, p.d_S, p.d_cls, p.d_dirs, p.d_Ypart, p.d_fold_cls, p.d_proj_cls};
         for (void* b : bufs)
             if (b) cudaFree(b);
     }
@@ -284,58 +284,84 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     }
     p.Q_pad = p.pair_srp ? (p.Q_eff + 255) / 256 * 256 : (p.Q_eff + 127) / 128 * 128;
 
-    // ---- antipodal folding of the SRP GEMM (R22): class c' is the antipode of class c when its tau row is
-    // the bitwise negation of c's (far field on a centrally symmetric grid: eq. 2 is odd in s_q, so every product
-    // and sum negates exactly).  Then W_c' = conj W_c (eq. 4) and one fold row gives both scores.
-    std::vector<int> fold_m, fold_p;
-    {
-        const char* e = getenv("SVDPHAT_FOLD");
-        const bool want = (e ? atoi(e) != 0 : true) && p.pair_srp && (p.methods & SVDPHAT_METHOD_SRP);
-        if (want) {
-            auto row_hash = [&](const double* t) {
-                const unsigned char* b = reinterpret_cast<const unsigned char*>(t);
-                uint64_t hsh = 1469598103934665603ull;
-                for (size_t i = 0; i < (size_t)P * 8; ++i) hsh = (hsh ^ b[i]) * 1099511628211ull;
-                return hsh;
-            };
-            std::unordered_map<uint64_t, std::vector<int>> by_hash;
-            for (int c = 0; c < p.Q_eff; ++c) by_hash[row_hash(&tau[(size_t)p.rep_q[c] * P])].push_back(c);
-            std::vector<double> neg(P);
-            std::vector<char> used(p.Q_eff, 0);
-            for (int c = 0; c < p.Q_eff; ++c) {
-                if (used[c]) continue;
-                const double* t = &tau[(size_t)p.rep_q[c] * P];
-                for (int i = 0; i < P; ++i) neg[i] = -t[i] + 0.0;              // +0.0: rows never hold -0
-                int partner = -1;
-                auto it = by_hash.find(row_hash(neg.data()));
-                if (it != by_hash.end())
-                    for (int c2 : it->second)
-                        if (c2 != c && !used[c2] &&
-                            std::memcmp(&tau[(size_t)p.rep_q[c2] * P], neg.data(), (size_t)P * 8) == 0) {
-                            partner = c2;
-                            break;
-                        }
-                used[c] = 1;
-                if (partner >= 0) used[partner] = 1;
-                fold_m.push_back(c);
-                fold_p.push_back(partner);
-            }
-            // fold only when it removes at least a quarter of the rows
-            p.fold = 4 * (int64_t)fold_m.size() <= 3 * (int64_t)p.Q_eff;
-        }
-    }
-    if (p.fold) {
-        p.fold_rows = (int)fold_m.size();
-        p.W_rows = (p.fold_rows + 255) / 256 * 256;
-        p.spc_W = 2 * ((p.L.U + 15) / 16);
-    } else {
-        p.W_rows = (p.Q_eff + 255) / 256 * 256;
-        p.spc_W = p.L.U / 8;
-    }
-    p.K_W = (int64_t)p.L.n_chunks * p.spc_W * 64;
     {
         const char* e = getenv("SVDPHAT_PAIR_PROJ");
         p.pair_proj = e ? atoi(e) != 0 : true;
+    }
+    // ---- antipodal class pairs (R22): class c' is the antipode of class c when its tau row is the bitwise
+    // negation of c's (far field on a centrally symmetric grid: eq. 2 is odd in s_q, so every product and sum
+    // negates exactly).  Then W_c' = conj W_c (eq. 4): one SRP fold row gives both scores, and W^H W is real, so
+    // the SVD's V can be taken real (the projection then folds the same way).  A class whose tau row is all zeros is
+    // its own antipode (a real W row).
+    std::vector<int> fold_m, fold_p;
+    bool all_paired = true;
+    {
+        auto row_hash = [&](const double* t) {
+            const unsigned char* b = reinterpret_cast<const unsigned char*>(t);
+            uint64_t hsh = 1469598103934665603ull;
+            for (size_t i = 0; i < (size_t)P * 8; ++i) hsh = (hsh ^ b[i]) * 1099511628211ull;
+            return hsh;
+        };
+        std::unordered_map<uint64_t, std::vector<int>> by_hash;
+        for (int c = 0; c < p.Q_eff; ++c) by_hash[row_hash(&tau[(size_t)p.rep_q[c] * P])].push_back(c);
+        std::vector<double> neg(P);
+        std::vector<char> used(p.Q_eff, 0);
+        for (int c = 0; c < p.Q_eff; ++c) {
+            if (used[c]) continue;
+            const double* t = &tau[(size_t)p.rep_q[c] * P];
+            bool zero = true;
+            for (int i = 0; i < P; ++i) {
+                neg[i] = -t[i] + 0.0;                                  // +0.0: rows never hold -0
+                zero = zero && t[i] == 0.0;
+            }
+            int partner = -1;
+            auto it = by_hash.find(row_hash(neg.data()));
+            if (it != by_hash.end())
+                for (int c2 : it->second)
+                    if (c2 != c && !used[c2] &&
+                        std::memcmp(&tau[(size_t)p.rep_q[c2] * P], neg.data(), (size_t)P * 8) == 0) {
+                        partner = c2;
+                        break;
+                    }
+            used[c] = 1;
+            if (partner >= 0) used[partner] = 1;
+            all_paired = all_paired && (partner >= 0 || zero);
+            fold_m.push_back(c);
+            fold_p.push_back(partner);
+        }
+    }
+    const bool few_rows = 4 * (int64_t)fold_m.size() <= 3 * (int64_t)p.Q_eff;   // folding removes >= 1/4 of rows
+    {
+        const char* e = getenv("SVDPHAT_FOLD");
+        p.fold = (e ? atoi(e) != 0 : true) && p.pair_srp && (p.methods & SVDPHAT_METHOD_SRP) && few_rows;
+        const char* e2 = getenv("SVDPHAT_SVD_FOLD");
+        p.svd_fold = (e2 ? atoi(e2) != 0 : true) && p.pair_proj && (p.methods & SVDPHAT_METHOD_SVD) && few_rows &&
+                     all_paired;
+    }
+    p.fold_rows = (int)fold_m.size();
+    p.spc_F = 2 * ((p.L.U + 15) / 16);
+    p.K_F = (int64_t)p.L.n_chunks * p.spc_F * 64;
+    if (p.fold) {
+        p.W_rows = (p.fold_rows + 255) / 256 * 256;
+        p.spc_W = p.spc_F;
+        p.K_W = p.K_F;
+    } else {
+        p.W_rows = (p.Q_eff + 255) / 256 * 256;
+        p.spc_W = p.L.U / 8;
+        p.K_W = p.L.K_total;
+    }
+    if (p.svd_fold) {
+        // real basis of the class rows: a pair (c, c') -> sqrt2 Re W_c, sqrt2 Im W_c; a self-antipodal c -> W_c
+        for (size_t r = 0; r < fold_m.size(); ++r) {
+            p.rb_cls.push_back(fold_m[r]);
+            p.rb_partner.push_back(fold_p[r]);
+            p.rb_kind.push_back(fold_p[r] >= 0 ? 0 : 2);
+            if (fold_p[r] >= 0) {
+                p.rb_cls.push_back(fold_m[r]);
+                p.rb_partner.push_back(fold_p[r]);
+                p.rb_kind.push_back(1);
+            }
+        }
     }
 
     // ---- device tables
@@ -407,7 +433,7 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     if (p.methods & SVDPHAT_METHOD_SVD) {
         st = setup_svd_operands(p, d_tau, d->rank_D);
         if (st != SVDPHAT_OK) return st;
-        if (!encode_2d(&p.tm_V, p.d_V16, p.V_rows, p.L.K_total, 128))
+        if (!encode_2d(&p.tm_V, p.d_V16, p.V_rows, p.svd_fold ? p.K_F : p.L.K_total, 128))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(V) failed");
         if (!encode_2d(&p.tm_R, p.d_R16, p.Q_pad, p.K2, 128))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(R) failed");

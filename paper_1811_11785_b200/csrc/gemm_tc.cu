@@ -45,8 +45,9 @@ struct GemmParams {
     int prefetch;                          // 0 none, 1 L2 prefetch of the next chunk's phasors, 2 same evict_last
     int bn;                                // frames per tile of the CTA-pair kernel (multiple of 32, <= 256)
     int c_lo, c_hi;                        // active bin-chunk range (band limit, NEXT-3); producer modes only
-    const int* fold_cls;                   // folded SRP (FOLD kernels): [2][fold_rows] classes of a - b / a + b
+    const int* fold_cls;                   // FOLD kernels: [2][fold_rows] output columns of the two results of a row
     int fold_rows;
+    int fold_ab;                           // FOLD store: 0 -> (a - b, a + b) (SRP), 1 -> (a, b) (real-V projection)
     int dbg;                               // timing experiments only (SVDPHAT_GEMM_DBG): 1 producer writes zeros,
                                            // 2 TMA re-loads one W tile (results invalid)
 };
@@ -657,8 +658,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                             float* zf = Zs + (int64_t)(f0 + jj) * p.ldz;
                             if (FOLD) {
                                 const float a = __uint_as_float(r[jj]), b = __uint_as_float(rb[jj]);
-                                zf[cls_m] = a - b;
-                                if (cls_p >= 0) zf[cls_p] = a + b;
+                                if (p.fold_ab) {
+                                    zf[cls_m] = a;
+                                    zf[cls_p] = b;
+                                } else {
+                                    zf[cls_m] = a - b;
+                                    if (cls_p >= 0) zf[cls_p] = a + b;
+                                }
                             } else {
                                 zf[row] = __uint_as_float(r[jj]);
                             }
@@ -1022,7 +1028,7 @@ ProjShape proj_shape(const Plan& p, int F) {
     const int units = sh.m_tiles * n_tiles;
     const int slots = sh.pair ? p.num_sms / 2 : p.num_sms;
     const int nc = p.c_hi - p.c_lo;
-    const double slabs = (double)nc * (p.L.U / 8);
+    const double slabs = (double)nc * (p.svd_fold ? p.spc_F : p.L.U / 8);
     double best_t = 1e300;
     sh.ksplit = 1;
     for (int S = 1; S <= p.zsplit_max && S <= nc; ++S) {
@@ -1088,9 +1094,18 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
         gp.m_tiles = p.W_rows / (p.pair_srp ? 256 : BM);
     } else if (mode == 1) {
         A = &p.tm_V;
-        gp.n_slabs = (int)(p.L.K_total / BK);
+        if (p.svd_fold) {              // real V: fold rows d, accumulators a -> Z_r (column d), b -> Z_i (Dh + d)
+            gp.n_slabs = (int)(p.K_F / BK);
+            gp.spc = p.spc_F;
+            gp.rows_valid = p.D;
+            gp.fold_cls = p.d_proj_cls;
+            gp.fold_rows = p.D;
+            gp.fold_ab = 1;
+        } else {
+            gp.n_slabs = (int)(p.L.K_total / BK);
+            gp.rows_valid = 2 * p.Dh;
+        }
         gp.m_tiles = (2 * p.Dh) / BM;
-        gp.rows_valid = 2 * p.Dh;
     } else {                           // 2: SVD search + argmax; 4: its power map Re{Dhat Zhat}[f][class] -> S
         A = &p.tm_R;
         B = &p.tm_Zs;
@@ -1121,7 +1136,7 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
             gp.m_tiles = sh.m_tiles;
             const int units = gp.m_tiles * gp.n_tiles * gp.ksplit;
             if (units == 0) return cudaSuccess;
-            return launch_pair<1>(p, *A, *B, gp, units < npairs ? units : npairs, false, s);
+            return launch_pair<1>(p, *A, *B, gp, units < npairs ? units : npairs, p.svd_fold, s);
         }
         tiles *= gp.ksplit;
     }

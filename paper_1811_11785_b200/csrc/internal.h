@@ -55,9 +55,17 @@ struct Plan {
     int fold_rows = 0;            // rows of the folded W (classes paired with their antipode, or alone)
     int* d_fold_cls = nullptr;    // [2][fold_rows]: class of a - b, class of a + b (-1: none)
     int W_rows = 0;               // rows of W16 (multiple of 256 for the pair kernel)
+    int64_t K_F = 0;              // fold contraction length (n_chunks * spc_F * 64)
+    int spc_F = 0;                // fold slabs per bin chunk (2 * ceil(U/16))
+    // SVD with a real V (R22): when every class has its antipode (or a zero tau row), W^H W is real; the
+    // SVD is taken of the real W~ = T W (rows sqrt2 Re W_c, sqrt2 Im W_c per pair, W_c for a real row), so V is real
+    // and Z_r = V^T x_r, Z_i = V^T x_i: the projection runs as a fold GEMM on D rows (a -> Z_r, b -> Z_i).
+    bool svd_fold = false;
+    std::vector<int> rb_cls, rb_partner, rb_kind;   // real basis row i: class, antipode (-1), kind 0 Re / 1 Im / 2 real
+    int* d_proj_cls = nullptr;    // [2][D]: Z columns of a (d) and b (Dh + d) for the folded projection
     int64_t K_W = 0;              // contraction length of W16
     int spc_W = 0;                // W16 slabs per bin chunk
-    __half* d_V16 = nullptr;      // [2*Dh][K_total]
+    __half* d_V16 = nullptr;      // [V_rows][K_total], or [V_rows][K_F] folded (svd_fold: one row per d)
     __half* d_R16 = nullptr;      // [Q_pad][K2]
     int* d_rep = nullptr;         // [Q_eff]
     float* d_delay = nullptr;     // [Q][M]  relative arrival delays (samples)

@@ -11,6 +11,7 @@
 //          V_D = W^H U_D S_D^{-1} (eq. 10) formed column-chunk-wise with cuBLAS ZGEMM on generated W chunks.
 //          Dictionary rows D_q = (U S)_q (eq. 13) normalised -> split FP16 [hi | lo | hi].
 #include <cublas_v2.h>
+#include <cuComplex.h>
 #include <cuda_fp16.h>
 #include <cusolverDn.h>
 
@@ -167,6 +168,109 @@ __global__ void pack_v16_kernel(const cuDoubleComplex* __restrict__ Vc, int C, i
     zi[ki] = __double2half(scale * v.x);
 }
 
+// ---------------------------------------------------------------- real-basis SVD (svd_fold, R22)
+// Real basis row i = sum over its class rows x of coef_i[x] W'_x: kind 0 (W_c + W_c')/sqrt2 = sqrt2 Re W_c, kind 1
+// (W_c - W_c')/(sqrt2 j) = sqrt2 Im W_c, kind 2 W_c (real row).  T with these rows is unitary and T W' is real.
+__device__ __forceinline__ int rb_terms(int kind, int c, int cp, int* cls, cuDoubleComplex* coef) {
+    const double h = 0.70710678118654752440;
+    if (kind == 2) {
+        cls[0] = c;
+        coef[0] = make_cuDoubleComplex(1.0, 0.0);
+        return 1;
+    }
+    cls[0] = c;
+    cls[1] = cp;
+    coef[0] = kind == 0 ? make_cuDoubleComplex(h, 0.0) : make_cuDoubleComplex(0.0, -h);
+    coef[1] = kind == 0 ? make_cuDoubleComplex(h, 0.0) : make_cuDoubleComplex(0.0, h);
+    return 2;
+}
+
+// G~ = T G' T^H (real symmetric), lower triangle column-major, from the Hermitian G' (lower triangle column-major)
+__global__ void rgram_kernel(const cuDoubleComplex* __restrict__ G, int n, const int* __restrict__ rb_cls,
+                             const int* __restrict__ rb_partner, const int* __restrict__ rb_kind, double* __restrict__ Gr) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int j = blockIdx.y;
+    if (i >= n || i < j) return;
+    int ci[2], cj[2];
+    cuDoubleComplex ai[2], aj[2];
+    const int ni = rb_terms(rb_kind[i], rb_cls[i], rb_partner[i], ci, ai);
+    const int nj = rb_terms(rb_kind[j], rb_cls[j], rb_partner[j], cj, aj);
+    double acc = 0.0;
+    for (int x = 0; x < ni; ++x)
+        for (int y = 0; y < nj; ++y) {
+            const int a = ci[x], b = cj[y];
+            const cuDoubleComplex g = a >= b ? G[(int64_t)b * n + a] : cuConj(G[(int64_t)a * n + b]);
+            // Re{ ai conj(aj) g }
+            acc += cuCreal(cuCmul(cuCmul(ai[x], cuConj(aj[y])), g));
+        }
+    Gr[(int64_t)j * n + i] = acc;
+}
+
+// B~[i][d] (column-major n x D) = sqrt(n_i) U~[i][jd] / sqrt(lambda_jd)
+__global__ void rbmat_kernel(const double* __restrict__ Ur, const double* __restrict__ lam, const int* __restrict__ cnt,
+                             const int* __restrict__ rb_cls, int n, int D, double* __restrict__ B) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int d = blockIdx.y;
+    if (i >= n) return;
+    const int jd = n - 1 - d;
+    B[(int64_t)d * n + i] = sqrt((double)cnt[rb_cls[i]] / lam[jd]) * Ur[(int64_t)jd * n + i];
+}
+
+// W~ chunk, column-major n x C (real): columns c0..c0+C-1 of eq. 8 in the real basis
+__global__ void rwchunk_kernel(const double* __restrict__ tau, const int* __restrict__ rb_cls,
+                               const int* __restrict__ rb_kind, int n, int P, int N, int Kb, int64_t c0, int C,
+                               double* __restrict__ Wc) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int cc = blockIdx.y;
+    if (i >= n) return;
+    const int64_t col = c0 + cc;
+    const int p = (int)(col / Kb), k = (int)(col % Kb);
+    double sn, cs;
+    sincospi(2.0 * (double)k * tau[(int64_t)rb_cls[i] * P + p] / (double)N, &sn, &cs);
+    const int kind = rb_kind[i];
+    const double r2 = 1.41421356237309504880;
+    Wc[(int64_t)cc * n + i] = kind == 0 ? r2 * cs : (kind == 1 ? r2 * sn : cs);
+}
+
+// real V chunk (column-major C x D) -> folded V16 row d: the same value in the Re slab (-> Z_r) and the Im slab (-> Z_i)
+__global__ void pack_v16f_kernel(const double* __restrict__ Vc, int C, int64_t c0, int M, int Mi, int Kb, int bpc,
+                                 int SP, int64_t K_F, double scale, __half* __restrict__ V16) {
+    const int cc = blockIdx.x * blockDim.x + threadIdx.x;
+    const int d = blockIdx.y;
+    if (cc >= C) return;
+    const int64_t col = c0 + cc;
+    const int p = (int)(col / Kb), k = (int)(col % Kb);
+    int i = 0, rem = p;
+    while (rem >= M - 1 - i) {
+        rem -= M - 1 - i;
+        ++i;
+    }
+    const int pi = pair_index(i, i + 1 + rem, Mi);
+    const __half v = __double2half(scale * Vc[(int64_t)d * C + cc]);
+    __half* row = V16 + (int64_t)d * K_F;
+    row[kappa_fold(pi, k, 0, bpc, SP)] = v;
+    row[kappa_fold(pi, k, 1, bpc, SP)] = v;
+}
+
+// class-basis eigenvectors U' = T^H U~ (columns jd >= n - D) into the complex n x n buffer read by pack_r16_kernel:
+// pair rows (ip, im): U'_c = (U~_ip + j U~_im)/sqrt2, U'_c' = (U~_ip - j U~_im)/sqrt2; a real row: U'_c = U~_ip
+__global__ void ucplx_kernel(const double* __restrict__ Ur, const int* __restrict__ cls_ip,
+                             const int* __restrict__ cls_im, const int* __restrict__ cls_sign, int n, int D,
+                             cuDoubleComplex* __restrict__ Uc) {
+    const int a = blockIdx.x * blockDim.x + threadIdx.x;
+    const int d = blockIdx.y;
+    if (a >= n) return;
+    const int jd = n - 1 - d;
+    const double up = Ur[(int64_t)jd * n + cls_ip[a]];
+    if (cls_im[a] < 0) {
+        Uc[(int64_t)jd * n + a] = make_cuDoubleComplex(up, 0.0);
+    } else {
+        const double h = 0.70710678118654752440;
+        const double um = Ur[(int64_t)jd * n + cls_im[a]];
+        Uc[(int64_t)jd * n + a] = make_cuDoubleComplex(h * up, h * cls_sign[a] * um);
+    }
+}
+
 // R16 row a: Rhat_a = normalise(U'[a][jd] sqrt(lambda_d)) -> [hi(Re) hi(-Im) | lo(Re) lo(-Im) | hi(Re) hi(-Im)]
 __global__ void pack_r16_kernel(const cuDoubleComplex* __restrict__ Uv, const double* __restrict__ lam, int n, int D,
                                 int Dh, int K2, __half* __restrict__ R16) {
@@ -235,6 +339,84 @@ struct DevBuf {
 };
 }  // namespace
 
+// svd_fold: V_D = W~^T N^1/2 U~ Lambda^{-1/2} (real; DGEMM on generated W~ chunks) packed as fold rows, and the
+// class-basis eigenvectors U' = T^H U~ written into Uc for the dictionary rows.
+static svdphat_status setup_real_v(Plan& p, const double* d_tau_cls, int n, int D, const double* Ur, const double* lam,
+                                   const int* cnt, const int* d_rb, cuDoubleComplex* Uc) {
+    DevBuf B, Wc, Vc, maps, pc;
+    SVD_CUDA_TRY(cudaMalloc(&B.ptr, (size_t)n * D * sizeof(double)));
+    {
+        dim3 grid(cdiv(n, 128), D);
+        rbmat_kernel<<<grid, 128>>>(Ur, lam, cnt, d_rb, n, D, (double*)B.ptr);
+        SVD_CUDA_TRY(cudaGetLastError());
+    }
+    p.V_rows = (D + 255) / 256 * 256;
+    p.bytes_V = (int64_t)p.V_rows * p.K_F * 2;
+    SVD_CUDA_TRY(cudaMalloc(&p.d_V16, p.bytes_V));
+    SVD_CUDA_TRY(cudaMemset(p.d_V16, 0, p.bytes_V));
+    int64_t CH = std::max<int64_t>(256, std::min<int64_t>(p.PK, (int64_t)(1ll << 30) / ((int64_t)n * 8)));
+    CH = std::min<int64_t>(CH, 16384);
+    SVD_CUDA_TRY(cudaMalloc(&Wc.ptr, (size_t)n * CH * sizeof(double)));
+    SVD_CUDA_TRY(cudaMalloc(&Vc.ptr, (size_t)CH * D * sizeof(double)));
+    cublasHandle_t bh = nullptr;
+    if (cublasCreate(&bh) != CUBLAS_STATUS_SUCCESS) {
+        set_error("cublasCreate failed");
+        return SVDPHAT_CUDA;
+    }
+    const double one = 1.0, zero = 0.0;
+    const double scale = std::sqrt((double)p.PK);
+    for (int64_t c0 = 0; c0 < p.PK; c0 += CH) {
+        const int C = (int)std::min<int64_t>(CH, p.PK - c0);
+        dim3 g1(cdiv(n, 128), C);
+        rwchunk_kernel<<<g1, 128>>>(d_tau_cls, d_rb, d_rb + 2 * n, n, p.P, p.N, p.Kb, c0, C, (double*)Wc.ptr);
+        cublasStatus_t bs = cublasDgemm(bh, CUBLAS_OP_T, CUBLAS_OP_N, C, D, n, &one, (const double*)Wc.ptr, n,
+                                        (const double*)B.ptr, n, &zero, (double*)Vc.ptr, C);
+        if (bs != CUBLAS_STATUS_SUCCESS) {
+            cublasDestroy(bh);
+            set_error("cublasDgemm failed: " + std::to_string((int)bs));
+            return SVDPHAT_CUDA;
+        }
+        dim3 g2(cdiv(C, 128), D);
+        pack_v16f_kernel<<<g2, 128>>>((const double*)Vc.ptr, C, c0, p.M, p.L.Mi, p.Kb, p.L.bpc, p.spc_F / 2, p.K_F,
+                                      scale, p.d_V16);
+    }
+    cublasDestroy(bh);
+    SVD_CUDA_TRY(cudaGetLastError());
+    // class -> its real rows: Re row, Im row (-1 for a real row), sign of the Im part (+ for c, - for the antipode)
+    std::vector<int> ip(n, -1), im(n, -1), sg(n, 1);
+    for (int i = 0; i < n; ++i) {
+        const int c = p.rb_cls[i], cp = p.rb_partner[i];
+        if (p.rb_kind[i] == 2) {
+            ip[c] = i;
+        } else if (p.rb_kind[i] == 0) {
+            ip[c] = ip[cp] = i;
+            sg[cp] = -1;
+        } else {
+            im[c] = im[cp] = i;
+        }
+    }
+    SVD_CUDA_TRY(cudaMalloc(&maps.ptr, (size_t)3 * n * sizeof(int)));
+    int* d_maps = (int*)maps.ptr;
+    SVD_CUDA_TRY(cudaMemcpy(d_maps, ip.data(), (size_t)n * sizeof(int), cudaMemcpyHostToDevice));
+    SVD_CUDA_TRY(cudaMemcpy(d_maps + n, im.data(), (size_t)n * sizeof(int), cudaMemcpyHostToDevice));
+    SVD_CUDA_TRY(cudaMemcpy(d_maps + 2 * n, sg.data(), (size_t)n * sizeof(int), cudaMemcpyHostToDevice));
+    {
+        dim3 grid(cdiv(n, 128), D);
+        ucplx_kernel<<<grid, 128>>>(Ur, d_maps, d_maps + n, d_maps + 2 * n, n, D, Uc);
+        SVD_CUDA_TRY(cudaGetLastError());
+    }
+    // Z columns of the fold accumulators: a (Z_r) -> d, b (Z_i) -> Dh + d
+    std::vector<int> cols(2 * (size_t)D);
+    for (int d = 0; d < D; ++d) {
+        cols[d] = d;
+        cols[D + d] = p.Dh + d;
+    }
+    SVD_CUDA_TRY(cudaMalloc(&p.d_proj_cls, cols.size() * sizeof(int)));
+    SVD_CUDA_TRY(cudaMemcpy(p.d_proj_cls, cols.data(), cols.size() * sizeof(int), cudaMemcpyHostToDevice));
+    SVD_CUDA_TRY(cudaDeviceSynchronize());
+    return SVDPHAT_OK;
+}
+
 svdphat_status setup_svd_operands(Plan& p, const double* d_tau_cls, int rank_D) {
     const int n = p.Q_eff;
     DevBuf G, lam, cnt, work, info, B, Wc, Vc;
@@ -248,36 +430,55 @@ svdphat_status setup_svd_operands(Plan& p, const double* d_tau_cls, int rank_D) 
         gram_kernel<<<grid, 128>>>(d_tau_cls, (const int*)cnt.ptr, n, p.P, p.N, p.Kb, (cuDoubleComplex*)G.ptr);
         SVD_CUDA_TRY(cudaGetLastError());
     }
-    // ---- Hermitian eigendecomposition (float64, cuSOLVER)
+    // ---- eigendecomposition (float64, cuSOLVER): Hermitian G', or (svd_fold) the real symmetric G~ = T G' T^H
+    DevBuf Gr, rb;
+    int* d_rb = nullptr;                                     // [3][n] real basis: class, partner, kind
+    if (p.svd_fold) {
+        SVD_CUDA_TRY(cudaMalloc(&Gr.ptr, (size_t)n * n * sizeof(double)));
+        SVD_CUDA_TRY(cudaMalloc(&rb.ptr, (size_t)3 * n * sizeof(int)));
+        d_rb = (int*)rb.ptr;
+        SVD_CUDA_TRY(cudaMemcpy(d_rb, p.rb_cls.data(), (size_t)n * sizeof(int), cudaMemcpyHostToDevice));
+        SVD_CUDA_TRY(cudaMemcpy(d_rb + n, p.rb_partner.data(), (size_t)n * sizeof(int), cudaMemcpyHostToDevice));
+        SVD_CUDA_TRY(cudaMemcpy(d_rb + 2 * n, p.rb_kind.data(), (size_t)n * sizeof(int), cudaMemcpyHostToDevice));
+        dim3 grid(cdiv(n, 128), n);
+        rgram_kernel<<<grid, 128>>>((const cuDoubleComplex*)G.ptr, n, d_rb, d_rb + n, d_rb + 2 * n, (double*)Gr.ptr);
+        SVD_CUDA_TRY(cudaGetLastError());
+    }
     cusolverDnHandle_t sh = nullptr;
     if (cusolverDnCreate(&sh) != CUSOLVER_STATUS_SUCCESS) {
         set_error("cusolverDnCreate failed");
         return SVDPHAT_CUDA;
     }
     int lwork = 0;
-    cusolverStatus_t cs = cusolverDnZheevd_bufferSize(sh, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
-                                                      (cuDoubleComplex*)G.ptr, n, (double*)lam.ptr, &lwork);
+    cusolverStatus_t cs =
+        p.svd_fold ? cusolverDnDsyevd_bufferSize(sh, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
+                                                 (double*)Gr.ptr, n, (double*)lam.ptr, &lwork)
+                   : cusolverDnZheevd_bufferSize(sh, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
+                                                 (cuDoubleComplex*)G.ptr, n, (double*)lam.ptr, &lwork);
     if (cs != CUSOLVER_STATUS_SUCCESS) {
         cusolverDnDestroy(sh);
-        set_error("cusolverDnZheevd_bufferSize failed: " + std::to_string((int)cs));
+        set_error("cusolver eigensolver bufferSize failed: " + std::to_string((int)cs));
         return SVDPHAT_CUDA;
     }
     {
-        cudaError_t e = cudaMalloc(&work.ptr, (size_t)lwork * sizeof(cuDoubleComplex));
+        cudaError_t e = cudaMalloc(&work.ptr, (size_t)lwork * (p.svd_fold ? sizeof(double) : sizeof(cuDoubleComplex)));
         if (e != cudaSuccess) {
             cusolverDnDestroy(sh);
             set_error("eigensolver workspace allocation failed");
             return SVDPHAT_ALLOC;
         }
     }
-    cs = cusolverDnZheevd(sh, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, (cuDoubleComplex*)G.ptr, n,
-                          (double*)lam.ptr, (cuDoubleComplex*)work.ptr, lwork, (int*)info.ptr);
+    cs = p.svd_fold ? cusolverDnDsyevd(sh, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n, (double*)Gr.ptr, n,
+                                       (double*)lam.ptr, (double*)work.ptr, lwork, (int*)info.ptr)
+                    : cusolverDnZheevd(sh, CUSOLVER_EIG_MODE_VECTOR, CUBLAS_FILL_MODE_LOWER, n,
+                                       (cuDoubleComplex*)G.ptr, n, (double*)lam.ptr, (cuDoubleComplex*)work.ptr,
+                                       lwork, (int*)info.ptr);
     cudaError_t se = cudaDeviceSynchronize();
     cusolverDnDestroy(sh);
     int hinfo = 0;
     cudaMemcpy(&hinfo, info.ptr, sizeof(int), cudaMemcpyDeviceToHost);
     if (cs != CUSOLVER_STATUS_SUCCESS || se != cudaSuccess || hinfo != 0) {
-        set_error("cusolverDnZheevd failed: status " + std::to_string((int)cs) + " info " + std::to_string(hinfo));
+        set_error("cusolver eigensolver failed: status " + std::to_string((int)cs) + " info " + std::to_string(hinfo));
         return SVDPHAT_NUMERIC;
     }
     cudaFree(work.ptr);
@@ -318,46 +519,52 @@ svdphat_status setup_svd_operands(Plan& p, const double* d_tau_cls, int rank_D) 
     p.Dh = (D + 63) / 64 * 64;
     p.K2 = 3 * 2 * p.Dh;
 
-    // ---- V_D = W^H N^1/2 U' Lambda^{-1/2}, column chunks of W, ZGEMM (float64)
-    SVD_CUDA_TRY(cudaMalloc(&B.ptr, (size_t)n * D * sizeof(cuDoubleComplex)));
-    {
-        dim3 grid(cdiv(n, 128), D);
-        bmat_kernel<<<grid, 128>>>((const cuDoubleComplex*)G.ptr, (const double*)lam.ptr, (const int*)cnt.ptr, n, D,
-                                   (cuDoubleComplex*)B.ptr);
-        SVD_CUDA_TRY(cudaGetLastError());
-    }
-    p.V_rows = p.pair_proj ? (2 * p.Dh + 255) / 256 * 256 : 2 * p.Dh;
-    p.bytes_V = (int64_t)p.V_rows * p.L.K_total * 2;
-    SVD_CUDA_TRY(cudaMalloc(&p.d_V16, p.bytes_V));
-    SVD_CUDA_TRY(cudaMemset(p.d_V16, 0, p.bytes_V));
-    int64_t CH = std::max<int64_t>(256, std::min<int64_t>(p.PK, (int64_t)(1ll << 30) / ((int64_t)n * 16)));
-    CH = std::min<int64_t>(CH, 16384);
-    SVD_CUDA_TRY(cudaMalloc(&Wc.ptr, (size_t)n * CH * sizeof(cuDoubleComplex)));
-    SVD_CUDA_TRY(cudaMalloc(&Vc.ptr, (size_t)CH * D * sizeof(cuDoubleComplex)));
-    cublasHandle_t bh = nullptr;
-    if (cublasCreate(&bh) != CUBLAS_STATUS_SUCCESS) {
-        set_error("cublasCreate failed");
-        return SVDPHAT_CUDA;
-    }
-    const cuDoubleComplex one = make_cuDoubleComplex(1, 0), zero = make_cuDoubleComplex(0, 0);
-    const double scale = std::sqrt((double)p.PK);
-    for (int64_t c0 = 0; c0 < p.PK; c0 += CH) {
-        const int C = (int)std::min<int64_t>(CH, p.PK - c0);
-        dim3 g1(cdiv(n, 128), C);
-        wchunk_kernel<<<g1, 128>>>(d_tau_cls, n, p.P, p.N, p.Kb, c0, C, (cuDoubleComplex*)Wc.ptr);
-        cublasStatus_t bs = cublasZgemm(bh, CUBLAS_OP_C, CUBLAS_OP_N, C, D, n, &one, (cuDoubleComplex*)Wc.ptr, n,
-                                        (cuDoubleComplex*)B.ptr, n, &zero, (cuDoubleComplex*)Vc.ptr, C);
-        if (bs != CUBLAS_STATUS_SUCCESS) {
-            cublasDestroy(bh);
-            set_error("cublasZgemm failed: " + std::to_string((int)bs));
+    if (p.svd_fold) {
+        svdphat_status st = setup_real_v(p, d_tau_cls, n, D, (const double*)Gr.ptr, (const double*)lam.ptr,
+                                         (const int*)cnt.ptr, d_rb, (cuDoubleComplex*)G.ptr);
+        if (st != SVDPHAT_OK) return st;
+    } else {
+        // ---- V_D = W^H N^1/2 U' Lambda^{-1/2}, column chunks of W, ZGEMM (float64)
+        SVD_CUDA_TRY(cudaMalloc(&B.ptr, (size_t)n * D * sizeof(cuDoubleComplex)));
+        {
+            dim3 grid(cdiv(n, 128), D);
+            bmat_kernel<<<grid, 128>>>((const cuDoubleComplex*)G.ptr, (const double*)lam.ptr, (const int*)cnt.ptr, n, D,
+                                       (cuDoubleComplex*)B.ptr);
+            SVD_CUDA_TRY(cudaGetLastError());
+        }
+        p.V_rows = p.pair_proj ? (2 * p.Dh + 255) / 256 * 256 : 2 * p.Dh;
+        p.bytes_V = (int64_t)p.V_rows * p.L.K_total * 2;
+        SVD_CUDA_TRY(cudaMalloc(&p.d_V16, p.bytes_V));
+        SVD_CUDA_TRY(cudaMemset(p.d_V16, 0, p.bytes_V));
+        int64_t CH = std::max<int64_t>(256, std::min<int64_t>(p.PK, (int64_t)(1ll << 30) / ((int64_t)n * 16)));
+        CH = std::min<int64_t>(CH, 16384);
+        SVD_CUDA_TRY(cudaMalloc(&Wc.ptr, (size_t)n * CH * sizeof(cuDoubleComplex)));
+        SVD_CUDA_TRY(cudaMalloc(&Vc.ptr, (size_t)CH * D * sizeof(cuDoubleComplex)));
+        cublasHandle_t bh = nullptr;
+        if (cublasCreate(&bh) != CUBLAS_STATUS_SUCCESS) {
+            set_error("cublasCreate failed");
             return SVDPHAT_CUDA;
         }
-        dim3 g2(cdiv(C, 128), D);
-        pack_v16_kernel<<<g2, 128>>>((const cuDoubleComplex*)Vc.ptr, C, D, p.Dh, c0, p.M, p.L.Mi, p.Kb, p.L.bpc,
-                                     p.L.U, p.L.K_total, scale, p.d_V16);
+        const cuDoubleComplex one = make_cuDoubleComplex(1, 0), zero = make_cuDoubleComplex(0, 0);
+        const double scale = std::sqrt((double)p.PK);
+        for (int64_t c0 = 0; c0 < p.PK; c0 += CH) {
+            const int C = (int)std::min<int64_t>(CH, p.PK - c0);
+            dim3 g1(cdiv(n, 128), C);
+            wchunk_kernel<<<g1, 128>>>(d_tau_cls, n, p.P, p.N, p.Kb, c0, C, (cuDoubleComplex*)Wc.ptr);
+            cublasStatus_t bs = cublasZgemm(bh, CUBLAS_OP_C, CUBLAS_OP_N, C, D, n, &one, (cuDoubleComplex*)Wc.ptr, n,
+                                            (cuDoubleComplex*)B.ptr, n, &zero, (cuDoubleComplex*)Vc.ptr, C);
+            if (bs != CUBLAS_STATUS_SUCCESS) {
+                cublasDestroy(bh);
+                set_error("cublasZgemm failed: " + std::to_string((int)bs));
+                return SVDPHAT_CUDA;
+            }
+            dim3 g2(cdiv(C, 128), D);
+            pack_v16_kernel<<<g2, 128>>>((const cuDoubleComplex*)Vc.ptr, C, D, p.Dh, c0, p.M, p.L.Mi, p.Kb, p.L.bpc,
+                                         p.L.U, p.L.K_total, scale, p.d_V16);
+        }
+        cublasDestroy(bh);
+        SVD_CUDA_TRY(cudaGetLastError());
     }
-    cublasDestroy(bh);
-    SVD_CUDA_TRY(cudaGetLastError());
     // ---- normalised dictionary rows (split FP16)
     p.bytes_R = (int64_t)p.Q_pad * p.K2 * 2;
     SVD_CUDA_TRY(cudaMalloc(&p.d_R16, p.bytes_R));

@@ -648,3 +648,41 @@ def test_antipodal_fold(M, monkeypatch):
     inf = plan.info()
     assert inf["srp_rows"] == inf["Q_classes"]
     plan.close()
+
+
+@pytest.mark.parametrize("M,planar", [(3, False), (7, True), (12, False), (20, False)])
+def test_real_v_projection(M, planar, monkeypatch):
+    """DESIGN.md R22 (SVD side): when every steering class has its antipode (or a zero tau row — the z axis of a
+    planar array), W^H W is real, the plan takes the SVD of the real W~ = T W, and Z = V^T X runs as a fold GEMM on
+    D rows.  Same D as the complex route and as the oracle, SVD-PHAT parity against the oracle's own SVD, and the same
+    DOAs as the complex-V plan (SVDPHAT_SVD_FOLD=0) up to near-ties."""
+    from workloads import geometry as G
+    from workloads import scenes as SC
+    rng = np.random.default_rng(777 + M)
+    mics = rng.uniform(-0.07, 0.07, (M, 3))
+    if planar:
+        mics[:, 2] = 0.0
+    pts = G.icosphere(3)
+    N, hop, F = 256, 128, 300
+    L = (F - 1) * hop + N
+    u = pts[rng.integers(len(pts))]
+    audio = SC.plane_wave_stream(rng, mics, 16000.0, 343.0, L, u, 10.0).astype(np.float32)
+    d_audio = torch.from_numpy(audio).to(DEV)
+    res, infos = {}, {}
+    for fold in ("1", "0"):
+        monkeypatch.setenv("SVDPHAT_SVD_FOLD", fold)
+        plan = S.Plan(mics, pts, 16000.0, 343.0, N, hop, "far", methods=("svd",), max_frames=F)
+        infos[fold] = plan.info()
+        res[fold] = _run(plan, type("W", (), {"channel_stride": L, "frame_stride": hop})(), "svd", d_audio, F)
+        plan.close()
+    assert infos["1"]["D"] == infos["0"]["D"]
+    assert infos["1"]["bytes_V"] < infos["0"]["bytes_V"]          # D fold rows instead of 2*D_h rows
+    tau = srp.tdoa(mics, pts, 16000.0, 343.0, "far")
+    fac = svd.svd_factors(tau, N, 1e-5)
+    assert fac["D"] == infos["1"]["D"]
+    x = srp.frames_to_x(srp.extract_frames(audio, F, M, N, L, hop))
+    keep = _check_degenerate(res["1"][0], res["1"][1], x)
+    P_, Y_at = PP.svd_reference(fac, tau, x[keep], N)
+    PP.compare(res["1"][0][keep], res["1"][1][keep], P_, Y_at, f"M={M} real V")
+    same = res["1"][0] == res["0"][0]
+    assert same.mean() >= 0.99
