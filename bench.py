@@ -291,7 +291,7 @@ def main() -> None:
             "flops_basis": f"4*srp_rows*PK*F, srp_rows={info['srp_rows']} (Q={info['Q']}, antipodal fold)",
             "flops_per_launch": flops, "peak_src": pk["src"] + " bf16_tflops_sustained (fp16 = bf16 rate)"}
     proj_ms = svd_stage_ms.get("svd_proj", float("nan"))
-    svd_flops = 8.0 * info["D"] * info["PK"] * F
+    svd_flops = 4.0 * info["svd_rows"] * info["PK"] * F      # 8·D·PK (complex V) or 4·D·PK (real V, R22)
     roof_svd = {"kernel": "svd_proj (method=svd run)", "stage_ms": svd_stage_ms, "achieved_tflops": svd_flops / (proj_ms / 1e3) / 1e12,
                 "frac_tensor": svd_flops / (proj_ms / 1e3) / 1e12 / peak,
                 "bytes_per_launch": float(info["bytes_V"] + F * w.M * w.N * 4)}

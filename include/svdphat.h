@@ -75,6 +75,8 @@ typedef struct {
     double setup_seconds;      /* wall time of svdphat_plan_create                                              */
     int32_t srp_rows;          /* rows of the SRP GEMM: Q_classes, or the antipodal fold rows when the grid is
                                   centrally symmetric in tau (class pairs tau_c' = -tau_c; R22)        */
+    int32_t svd_rows;          /* rows of the SVD projection GEMM: 2*D (complex V, real-split) or D (real V when
+                                  every class has its antipode; R22); 0 if SVD not planned             */
 } svdphat_plan_info_t;
 
 /* Alg. 1 offline steps 1-3: TDOAs (eq. 1/2), W (eqs. 4, 8), SVD (eq. 10) with the rank rule
