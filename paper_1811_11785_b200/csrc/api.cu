@@ -145,7 +145,7 @@ struct svdphat_plan_s {
         if (p.ev_join2) cudaEventDestroy(p.ev_join2);
         void* bufs[] = {p.d_W16,   p.d_V16,   p.d_R16,   p.d_rep,   p.d_delay,     p.d_window,      p.d_twN,
                         p.d_P16,   p.d_keys,  p.d_Z32,   p.d_Zs16,  p.d_zflag,     p.d_stage,       p.d_doa_stage,
-                        p.d_score_stage, p.d_S, p.d_cls, p.d_dirs, p.d_Ypart, p.d_fold_cls, p.d_proj_cls};
+                        p.d_score_stage, p.d_S, p.d_cls, p.d_dirs, p.d_Ypart, p.d_fold_cls};
         for (void* b : bufs)
             if (b) cudaFree(b);
     }
@@ -433,7 +433,8 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     if (p.methods & SVDPHAT_METHOD_SVD) {
         st = setup_svd_operands(p, d_tau, d->rank_D);
         if (st != SVDPHAT_OK) return st;
-        if (!encode_2d(&p.tm_V, p.d_V16, p.V_rows, p.svd_fold ? p.K_F : p.L.K_total, 128))
+        if (!encode_2d(&p.tm_V, p.d_V16, p.V_rows, p.svd_fold ? p.K_F : p.L.K_total,
+                       p.pair_proj ? p.proj_nt / 2 : 128))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(V) failed");
         if (!encode_2d(&p.tm_R, p.d_R16, p.Q_pad, p.K2, 128))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(R) failed");

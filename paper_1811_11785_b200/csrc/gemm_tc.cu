@@ -45,9 +45,8 @@ struct GemmParams {
     int prefetch;                          // 0 none, 1 L2 prefetch of the next chunk's phasors, 2 same evict_last
     int bn;                                // frames per tile of the CTA-pair kernel (multiple of 32, <= 256)
     int c_lo, c_hi;                        // active bin-chunk range (band limit, NEXT-3); producer modes only
-    const int* fold_cls;                   // FOLD kernels: [2][fold_rows] output columns of the two results of a row
+    const int* fold_cls;                   // folded SRP (FOLD kernels): [2][fold_rows] classes of a - b / a + b
     int fold_rows;
-    int fold_ab;                           // FOLD store: 0 -> (a - b, a + b) (SRP), 1 -> (a, b) (real-V projection)
     int dbg;                               // timing experiments only (SVDPHAT_GEMM_DBG): 1 producer writes zeros,
                                            // 2 TMA re-loads one W tile (results invalid)
 };
@@ -73,6 +72,23 @@ __device__ __forceinline__ Unit unit_of(const GemmParams& p, int t) {
         u.k0 = u.c0 * p.spc;
         u.k1 = u.c1 * p.spc;
     }
+    return u;
+}
+
+// Work-unit order of the frames-on-M projection (gemm2f_kernel): split slowest, then V tile, frame tile fastest, so
+// the pairs in flight share one V slab range and the split's phasor records stay L2-resident across the V tiles.
+__device__ __forceinline__ Unit unit_of_f(const GemmParams& p, int t) {
+    Unit u;
+    const int per_s = p.m_tiles * p.n_tiles;
+    u.s = t / per_s;
+    const int r = t - u.s * per_s;
+    u.n = r / p.m_tiles;
+    u.m = r - u.n * p.m_tiles;
+    const int nc = p.c_hi - p.c_lo;
+    u.c0 = p.c_lo + (int)((int64_t)u.s * nc / p.ksplit);
+    u.c1 = p.c_lo + (int)((int64_t)(u.s + 1) * nc / p.ksplit);
+    u.k0 = u.c0 * p.spc;
+    u.k1 = u.c1 * p.spc;
     return u;
 }
 
@@ -658,13 +674,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                             float* zf = Zs + (int64_t)(f0 + jj) * p.ldz;
                             if (FOLD) {
                                 const float a = __uint_as_float(r[jj]), b = __uint_as_float(rb[jj]);
-                                if (p.fold_ab) {
-                                    zf[cls_m] = a;
-                                    zf[cls_p] = b;
-                                } else {
-                                    zf[cls_m] = a - b;
-                                    if (cls_p >= 0) zf[cls_p] = a + b;
-                                }
+                                zf[cls_m] = a - b;
+                                if (cls_p >= 0) zf[cls_p] = a + b;
                             } else {
                                 zf[row] = __uint_as_float(r[jj]);
                             }
@@ -709,6 +720,200 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
             const bool valid = f < p.F && tp < hb && !(p.dbg & 1);
             produce_x_pair<Mi, BPC, STAGES2, B2_BYTES, FOLD>(p, w, f, valid, sB, full, empty, stage, phase, row_off,
                                                              xr);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc_2sm<512>(tmem_base);
+    }
+}
+
+// ================================================================================================================
+// SVD projection on CTA pairs with frames on M (eq. 12): Z[f, r] = sum_kappa x16[f,kappa] V16[r,kappa].
+// A = this CTA's 128 frames of X from the producer warps (produce_x_pair), B = proj_nt rows of V16 per pair tile
+// (proj_nt/2 per CTA, 2-SM TMA), N = proj_nt chosen at plan creation to cover the V rows tightly (cfg3 real V:
+// 2 x 160 = 320 rows for D = 318, where 256-row M tiles needed 512).  The accumulator lane is a frame and its
+// columns are V rows, so each thread writes a contiguous segment of its frame's Z row.  FOLD (real V, R22): slabs
+// alternate Re (accumulator a -> Z_r, column d) and Im (b -> Z_i, column D_h + d).  Warps as gemm2_kernel; work
+// units in unit_of_f order.  (r01: before the converged-warp MMA issue this orientation was issue-bound at N = 160.)
+// ================================================================================================================
+template <int Mi, int BPC, bool FOLD>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
+    gemm2f_kernel(const __grid_constant__ CUtensorMap tmV, GemmParams p) {
+    constexpr int kUnitsRaw = (BPC == 4) ? Mi * (Mi - 1) / 2 : (Mi * (Mi - 1) / 2 + 1) / 2;
+    constexpr int kU = (kUnitsRaw + 7) / 8 * 8;
+    constexpr bool kHalfPair = FOLD && (kU % 16 == 8);
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint8_t* sX = smem;                                     // A: 128 frames x 64 K per stage
+    uint8_t* sV = smem + STAGES2 * A2_BYTES;                // B: nt/2 V rows x 64 K per stage (<= 16 KB)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sV + STAGES2 * B2_BYTES);
+    uint64_t* empty = full + STAGES2;
+    uint64_t* tfull = empty + STAGES2;
+    uint64_t* tempty = tfull + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+    const int units = p.m_tiles * p.n_tiles * p.ksplit;
+    const int nt = p.bn, hn = p.bn / 2;                     // V rows per pair tile / per CTA
+    const uint32_t idesc = umma_idesc_f16(256, (uint32_t)nt);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES2; ++s) {
+            mbar_init(&full[s], 1 + 2 * NPW2);              // leader's TMA (expect_tx) + producers of both CTAs
+            mbar_init(&empty[s], 1);
+        }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&tfull[a], 1);
+            mbar_init(&tempty[a], 8);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc_2sm<512>(tmem_slot);
+    if (warp == 1 && lane == 0) tma_prefetch_desc(&tmV);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint32_t bytes = 2u * (uint32_t)hn * BK * 2;
+            for (int t = pair; t < units; t += n_pairs) {
+                const Unit w = unit_of_f(p, t);
+                for (int ks = w.k0; ks < w.k1; ++ks) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
+                    tma_load_2d_2sm(sV + stage * B2_BYTES, &tmV, ks * BK, w.n * nt + (int)rank * hn, &full[stage]);
+                    if (++stage == STAGES2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader) {                                       // converged-warp MMA issue (see gemm2_kernel)
+            const uint64_t adesc0 = umma_desc_sw128(smem_u32(sX)), bdesc0 = umma_desc_sw128(smem_u32(sV));
+            int stage = 0;
+            uint32_t phase = 0;
+            int acc = 0;
+            uint32_t acc_phase = 0;
+            for (int t = pair; t < units; t += n_pairs) {
+                const Unit w = unit_of_f(p, t);
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                int local = 0;
+                for (int ks = w.k0; ks < w.k1; ++ks) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint64_t ad = adesc0 + (uint64_t)(stage * (A2_BYTES >> 4));
+                    const uint64_t bd = bdesc0 + (uint64_t)(stage * (B2_BYTES >> 4));
+                    if constexpr (FOLD) {
+                        const uint32_t d_tmem = tmem_base + (uint32_t)(local & 1) * BN;
+                        const bool half = kHalfPair && local >= p.spc - 2;
+                        umma_f16_2sm_warp(d_tmem, ad, bd, idesc, ks >= w.k0 + 2);
+                        umma_f16_2sm_warp(d_tmem, ad + 2, bd + 2, idesc, 1u);
+                        if (!half) {
+                            umma_f16_2sm_warp(d_tmem, ad + 4, bd + 4, idesc, 1u);
+                            umma_f16_2sm_warp(d_tmem, ad + 6, bd + 6, idesc, 1u);
+                        }
+                        if (++local == p.spc) local = 0;
+                    } else {
+                        const uint32_t d_tmem = tmem_base + acc * BN;
+                        const uint32_t acc0 = ks != w.k0;
+#pragma unroll
+                        for (int kk = 0; kk < BK / 16; ++kk)
+                            umma_f16_2sm_warp(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, kk ? 1u : acc0);
+                    }
+                    umma_commit_2sm_warp(&empty[stage], 0x3);
+                    if (++stage == STAGES2) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                umma_commit_2sm_warp(&tfull[acc], 0x3);
+                if (FOLD) {
+                    acc_phase ^= 1;
+                } else if (++acc == 2) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+            }
+        }
+    } else if (warp < 6) {
+        // epilogue: TMEM lane = frame, columns = V rows [n*nt, n*nt + nt) -> Z[s][f][...]
+        const int g = warp & 3;
+        const int half_z = p.ldz / 2;                       // D_h: Z_i columns start here
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int t = pair; t < units; t += n_pairs) {
+            const Unit w = unit_of_f(p, t);
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int f = w.m * 256 + (int)rank * 128 + g * 32 + lane;
+            float* zrow = p.Z + ((int64_t)w.s * p.F_pad + f) * p.ldz;
+#pragma unroll 1
+            for (int j0 = 0; j0 < nt; j0 += 32) {
+                uint32_t r[32], rb[32];
+                tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + acc * BN + j0, r);
+                if (FOLD) tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + BN + j0, rb);
+                tmem_ld_wait();
+                const int r0 = w.n * nt + j0;               // first V row (FOLD: d) of these 32 columns
+                if (f < p.F) {
+                    if (FOLD) {
+                        if (r0 < half_z) {                  // whole 32-row group inside [0, D_h): D_h % 64 == 0
+                            float4* za = reinterpret_cast<float4*>(zrow + r0);
+                            float4* zb = reinterpret_cast<float4*>(zrow + half_z + r0);
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                za[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                                    __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+                                zb[q] = make_float4(__uint_as_float(rb[4 * q]), __uint_as_float(rb[4 * q + 1]),
+                                                    __uint_as_float(rb[4 * q + 2]), __uint_as_float(rb[4 * q + 3]));
+                            }
+                        }
+                    } else if (r0 < p.ldz) {
+                        float4* z = reinterpret_cast<float4*>(zrow + r0);
+#pragma unroll
+                        for (int q = 0; q < 8; ++q)
+                            z[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                               __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+                    }
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
+            if (FOLD) {
+                acc_phase ^= 1;
+            } else if (++acc == 2) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    } else {
+        const int tp = (warp - 6) * 32 + lane;              // frame row of this CTA's half tile: 0..127
+        const uint32_t row_off = (uint32_t)((tp >> 3) * 1024 + (tp & 7) * 128);
+        const uint32_t xr = (uint32_t)(tp & 7);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = pair; t < units; t += n_pairs) {
+            const Unit w = unit_of_f(p, t);
+            const int f = w.m * 256 + (int)rank * 128 + tp;
+            produce_x_pair<Mi, BPC, STAGES2, A2_BYTES, FOLD>(p, w, f, f < p.F, sX, full, empty, stage, phase,
+                                                             row_off, xr);
         }
     }
 
@@ -971,6 +1176,8 @@ static cudaError_t set_attr_pair() {
     if ((e = cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, 1, false>, attr, sm))) return e;
     if ((e = cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, 0, true>, attr, sm))) return e;
     if ((e = cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, 1, true>, attr, sm))) return e;
+    if ((e = cudaFuncSetAttribute(gemm2f_kernel<Mi, BPC, false>, attr, sm))) return e;
+    if ((e = cudaFuncSetAttribute(gemm2f_kernel<Mi, BPC, true>, attr, sm))) return e;
     return cudaFuncSetAttribute(gemm3_kernel<Mi, BPC>, attr, SMEM3_BYTES);
 }
 
@@ -1023,9 +1230,10 @@ static cudaError_t launch_one(const CUtensorMap& A, const CUtensorMap& B, const 
 ProjShape proj_shape(const Plan& p, int F) {
     ProjShape sh;
     sh.pair = p.pair_proj;
-    const int n_tiles = (F + BN - 1) / BN;
-    sh.m_tiles = sh.pair ? p.V_rows / 256 : (2 * p.Dh) / BM;
-    const int units = sh.m_tiles * n_tiles;
+    const int f_tiles = (F + BN - 1) / BN;
+    sh.m_tiles = sh.pair ? f_tiles : (2 * p.Dh) / BM;
+    sh.n_tiles = sh.pair ? p.proj_ntiles : f_tiles;
+    const int units = sh.m_tiles * sh.n_tiles;
     const int slots = sh.pair ? p.num_sms / 2 : p.num_sms;
     const int nc = p.c_hi - p.c_lo;
     const double slabs = (double)nc * (p.svd_fold ? p.spc_F : p.L.U / 8);
@@ -1098,9 +1306,6 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
             gp.n_slabs = (int)(p.K_F / BK);
             gp.spc = p.spc_F;
             gp.rows_valid = p.D;
-            gp.fold_cls = p.d_proj_cls;
-            gp.fold_rows = p.D;
-            gp.fold_ab = 1;
         } else {
             gp.n_slabs = (int)(p.L.K_total / BK);
             gp.rows_valid = 2 * p.Dh;
@@ -1132,11 +1337,27 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
         // split K (at chunk boundaries) to fill the SMs, deterministic partial buffers
         const ProjShape sh = proj_shape(p, F);
         gp.ksplit = sh.ksplit;
-        if (sh.pair) {
+        if (sh.pair) {                 // frames on M, V rows on N (gemm2f_kernel)
             gp.m_tiles = sh.m_tiles;
+            gp.n_tiles = sh.n_tiles;
+            gp.bn = p.proj_nt;
             const int units = gp.m_tiles * gp.n_tiles * gp.ksplit;
             if (units == 0) return cudaSuccess;
-            return launch_pair<1>(p, *A, *B, gp, units < npairs ? units : npairs, p.svd_fold, s);
+            const int pairs = units < npairs ? units : npairs;
+#define SVD_PROJ(MI, BP)                                                                                         \
+    if (p.L.Mi == MI) {                                                                                         \
+        if (p.svd_fold)                                                                                         \
+            gemm2f_kernel<MI, BP, true><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(*A, gp);                      \
+        else                                                                                                    \
+            gemm2f_kernel<MI, BP, false><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(*A, gp);                     \
+        return cudaGetLastError();                                                                              \
+    }
+            SVD_PROJ(4, 4)
+            SVD_PROJ(8, 4)
+            SVD_PROJ(16, 4)
+            SVD_PROJ(32, 2)
+#undef SVD_PROJ
+            return cudaErrorInvalidValue;
         }
         tiles *= gp.ksplit;
     }

@@ -62,7 +62,6 @@ struct Plan {
     // and Z_r = V^T x_r, Z_i = V^T x_i: the projection runs as a fold GEMM on D rows (a -> Z_r, b -> Z_i).
     bool svd_fold = false;
     std::vector<int> rb_cls, rb_partner, rb_kind;   // real basis row i: class, antipode (-1), kind 0 Re / 1 Im / 2 real
-    int* d_proj_cls = nullptr;    // [2][D]: Z columns of a (d) and b (Dh + d) for the folded projection
     int64_t K_W = 0;              // contraction length of W16
     int spc_W = 0;                // W16 slabs per bin chunk
     __half* d_V16 = nullptr;      // [V_rows][K_total], or [V_rows][K_F] folded (svd_fold: one row per d)
@@ -75,7 +74,9 @@ struct Plan {
     uint8_t* d_P16 = nullptr;     // phasors
     unsigned long long* d_keys = nullptr;  // [2][F_pad]: SRP keys, SVD search keys
     float* d_Z32 = nullptr;       // [zsplit_max][F_pad][2*Dh] partial Z of the split-K projection
-    int V_rows = 0;               // rows of V16 (2*Dh rounded up to 256 for the CTA-pair projection)
+    int V_rows = 0;               // rows of V16: proj_ntiles * proj_nt (pair projection) or 2*Dh (1-CTA)
+    int proj_nt = 0;              // V rows per pair tile of the frames-on-M projection (multiple of 32, <= 256)
+    int proj_ntiles = 0;          // V row tiles
     bool pair_proj = true;
     int zsplit_max = 1;
     // small batches: SRP as split-K partial power maps + sum/argmax (the argmax epilogue cannot split K)
@@ -155,7 +156,7 @@ cudaError_t launch_split_argmax(const Plan& p, int F, int S, cudaStream_t s);
 constexpr int MAX_KSPLIT = 32;               // cap on K splits (chunk ranges) of the store-mode GEMMs
 struct ProjShape {
     bool pair;
-    int m_tiles, ksplit;
+    int m_tiles, n_tiles, ksplit;   // pair: m = 256-frame tiles, n = proj_nt-row V tiles; 1-CTA: m = 128-row V tiles
 };
 ProjShape proj_shape(const Plan& p, int F);   // tiles and K splits of the SVD projection GEMM
 void set_band(Plan& p, int k_lo, int k_hi, const uint8_t* mask, int64_t mask_stride);

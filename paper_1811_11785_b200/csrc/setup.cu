@@ -16,6 +16,7 @@
 #include <cusolverDn.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <string>
 #include <vector>
@@ -330,6 +331,28 @@ svdphat_status setup_srp_operand(Plan& p, const double* d_tau_cls) {
     return SVDPHAT_OK;
 }
 
+// V row tiling of the frames-on-M pair projection: the fewest tiles of <= 256 rows (multiples of 32) covering `rows`
+// (SVDPHAT_PROJ_NT forces the tile height, for measurements).  cfg3: real V, D = 318 -> 2 x 160; complex V, 2*D_h =
+// 640 -> 3 x 224.
+static void choose_proj_tiles(Plan& p, int rows) {
+    if (!p.pair_proj) {
+        p.V_rows = rows;
+        return;
+    }
+    static const int forced = [] {
+        const char* e = getenv("SVDPHAT_PROJ_NT");
+        return e ? atoi(e) : 0;
+    }();
+    if (forced >= 32 && forced <= 256 && forced % 32 == 0) {
+        p.proj_nt = forced;
+        p.proj_ntiles = (rows + forced - 1) / forced;
+    } else {
+        p.proj_ntiles = (rows + 255) / 256;
+        p.proj_nt = ((rows + p.proj_ntiles - 1) / p.proj_ntiles + 31) / 32 * 32;
+    }
+    p.V_rows = p.proj_ntiles * p.proj_nt;
+}
+
 namespace {
 struct DevBuf {
     void* ptr = nullptr;
@@ -350,7 +373,7 @@ static svdphat_status setup_real_v(Plan& p, const double* d_tau_cls, int n, int 
         rbmat_kernel<<<grid, 128>>>(Ur, lam, cnt, d_rb, n, D, (double*)B.ptr);
         SVD_CUDA_TRY(cudaGetLastError());
     }
-    p.V_rows = (D + 255) / 256 * 256;
+    choose_proj_tiles(p, D);
     p.bytes_V = (int64_t)p.V_rows * p.K_F * 2;
     SVD_CUDA_TRY(cudaMalloc(&p.d_V16, p.bytes_V));
     SVD_CUDA_TRY(cudaMemset(p.d_V16, 0, p.bytes_V));
@@ -405,14 +428,6 @@ static svdphat_status setup_real_v(Plan& p, const double* d_tau_cls, int n, int 
         ucplx_kernel<<<grid, 128>>>(Ur, d_maps, d_maps + n, d_maps + 2 * n, n, D, Uc);
         SVD_CUDA_TRY(cudaGetLastError());
     }
-    // Z columns of the fold accumulators: a (Z_r) -> d, b (Z_i) -> Dh + d
-    std::vector<int> cols(2 * (size_t)D);
-    for (int d = 0; d < D; ++d) {
-        cols[d] = d;
-        cols[D + d] = p.Dh + d;
-    }
-    SVD_CUDA_TRY(cudaMalloc(&p.d_proj_cls, cols.size() * sizeof(int)));
-    SVD_CUDA_TRY(cudaMemcpy(p.d_proj_cls, cols.data(), cols.size() * sizeof(int), cudaMemcpyHostToDevice));
     SVD_CUDA_TRY(cudaDeviceSynchronize());
     return SVDPHAT_OK;
 }
@@ -532,7 +547,7 @@ svdphat_status setup_svd_operands(Plan& p, const double* d_tau_cls, int rank_D) 
                                        (cuDoubleComplex*)B.ptr);
             SVD_CUDA_TRY(cudaGetLastError());
         }
-        p.V_rows = p.pair_proj ? (2 * p.Dh + 255) / 256 * 256 : 2 * p.Dh;
+        choose_proj_tiles(p, 2 * p.Dh);
         p.bytes_V = (int64_t)p.V_rows * p.L.K_total * 2;
         SVD_CUDA_TRY(cudaMalloc(&p.d_V16, p.bytes_V));
         SVD_CUDA_TRY(cudaMemset(p.d_V16, 0, p.bytes_V));
