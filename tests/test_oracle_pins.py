@@ -353,3 +353,53 @@ def test_steering_classes_planar():
     reps = srp.steering_classes(tau)
     mirror = np.array([int(np.argmin(np.linalg.norm(grid - g * [1, 1, -1], axis=1))) for g in grid])
     assert sorted(reps.tolist()) == sorted(set(np.minimum(np.arange(len(grid)), mirror).tolist()))
+
+
+# ------------------------------------------------------------------ DESIGN.md R22: antipodal folding
+def _antipode_index(grid):
+    key = {r.tobytes(): i for i, r in enumerate(grid + 0.0)}
+    return np.array([key[((-r) + 0.0).tobytes()] for r in grid])
+
+
+def test_antipodal_fold_identity():
+    """Eq. 2 is odd in s_q, so on a centrally symmetric grid tau(-s) = -tau(s) bitwise, W_{q'} = conj(W_q) (eq. 4) and
+    eq. 9 for the pair follows from two real half products: Y_q = a - b, Y_q' = a + b with a = Re W_q . Re X and
+    b = Im W_q . Im X (the GPU's fold rows).  Checked against the oracle's complex BLAS product."""
+    rng = np.random.default_rng(22)
+    mics = rng.uniform(-0.06, 0.06, (7, 3))
+    grid = G.icosphere(2)
+    N = 128
+    tau = srp.tdoa_farfield(mics, grid, FS, C)
+    anti = _antipode_index(grid)
+    assert np.all(anti != np.arange(len(grid)))
+    for q in range(len(grid)):
+        assert np.array_equal(tau[anti[q]], -tau[q] + 0.0)
+    W = srp.steering_rows(tau, N)
+    assert np.max(np.abs(W[anti] - np.conj(W))) < 1e-12
+    x = srp.frames_to_x(rng.standard_normal((5, 7, N)))
+    Y = srp.srp_energy(tau, x, N)
+    a = np.real(W) @ np.real(x).T          # (Q, F)
+    b = np.imag(W) @ np.imag(x).T
+    scale = np.max(np.abs(Y))
+    assert np.max(np.abs((a - b).T - Y)) < 1e-10 * scale
+    assert np.max(np.abs((a + b).T - Y[:, anti])) < 1e-10 * scale
+
+
+def test_symmetric_grid_gram_is_real():
+    """With W_{q'} = conj(W_q) for every q, conj(W) = Pi W for the antipode permutation Pi, so W^H W is real and
+    T W (rows sqrt2 Re W_q, sqrt2 Im W_q per antipodal pair) is a real matrix with W's singular values: the SVD of
+    eq. 10 has a real V (R22, the GPU's real-V projection)."""
+    rng = np.random.default_rng(23)
+    mics = rng.uniform(-0.06, 0.06, (5, 3))
+    grid = G.icosphere(2)
+    N = 64
+    tau = srp.tdoa_farfield(mics, grid, FS, C)
+    W = srp.steering_rows(tau, N)
+    Gr = W.conj().T @ W
+    assert np.max(np.abs(Gr.imag)) < 1e-9 * np.max(np.abs(Gr))
+    anti = _antipode_index(grid)
+    prim = [q for q in range(len(grid)) if q < anti[q]]
+    Wt = np.concatenate([np.sqrt(2) * W[prim].real, np.sqrt(2) * W[prim].imag])
+    s_c = np.linalg.svd(W, compute_uv=False)
+    s_r = np.linalg.svd(Wt, compute_uv=False)
+    assert np.allclose(s_c, s_r, rtol=1e-9, atol=1e-9 * s_c[0])
