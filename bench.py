@@ -152,7 +152,7 @@ def run_reference(a) -> None:
         return
     from workloads import make
     w = make(a.cfg)
-    per = 32  # frames per step: each oracle pass regenerates the whole W (~13 s at cfg3), so 32 frames cost ~2
+    per = 32  # frames per step: every oracle pass regenerates the whole W (~13 s at cfg3), so 32 frames cost ~2 frames
     for _ in range(a.warmup):
         cpu_baseline(w, per)
     t = []
