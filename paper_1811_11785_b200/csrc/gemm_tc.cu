@@ -400,13 +400,13 @@ constexpr int SMEM2_BYTES = 1024 + STAGES2 * (A2_BYTES + B2_BYTES) + 256;
 // XB bytes, 8 units = one 64-element slab per stage).  The frame's phasors of the current chunk stay in registers.
 // (Register double-buffering of the next chunk was tried and removed: the apparent 'load cost' was power - zeroed
 // operands keep the clock high under the cap.)
-// FOLD (antipodal folding, internal.h): unit u's Re words go to the Re slab and its Im words to the Im slab of slab
-// pair u/16 (at byte 8*(u%16) of the swizzled row); the two stages of a slab pair fill together.
-template <int Mi, int BPC, int NSTAGES, int XB, bool FOLD = false>
+// FOLD (antipodal folding, internal.h): a stage holds slab pair u/16 - its Re slab at offset 0 and its Im slab at
+// SLAB - and unit u's Re / Im words go to byte 8*(u%16) of the swizzled row of each.
+template <int Mi, int BPC, int NSTAGES, int XB, bool FOLD = false, int SLAB = XB>
 __device__ __forceinline__ void produce_x_pair(const GemmParams& p, const Unit& w, int f, bool valid, uint8_t* sX,
                                                uint64_t* full, uint64_t* empty, int& stage, uint32_t& phase,
                                                uint32_t row_off, uint32_t xr) {
-    static_assert(!FOLD || NSTAGES % 2 == 0, "slab pairs need an even ring");
+    static_assert(!FOLD || XB == 2 * SLAB, "a fold stage holds a Re slab and an Im slab");
     constexpr PairTab<Mi> PT{};
     constexpr int kPairs = Mi * (Mi - 1) / 2;
     constexpr int kUnitsRaw = (BPC == 4) ? kPairs : (kPairs + 1) / 2;
@@ -437,10 +437,7 @@ __device__ __forceinline__ void produce_x_pair(const GemmParams& p, const Unit& 
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             if constexpr (FOLD) {
-                if ((u & 15) == 0) {
-                    mbar_wait(&empty[stage], phase ^ 1);
-                    mbar_wait(&empty[stage + 1], phase ^ 1);
-                }
+                if ((u & 15) == 0) mbar_wait(&empty[stage], phase ^ 1);
             } else {
                 if ((u & 7) == 0) mbar_wait(&empty[stage], phase ^ 1);
             }
@@ -483,17 +480,13 @@ __device__ __forceinline__ void produce_x_pair(const GemmParams& p, const Unit& 
                 } else {
                     const uint32_t pos = row_off + (((((uint32_t)u & 15u) >> 1) ^ xr) << 4);
                     st_shared_v4(smem_u32(sX + stage * XB) + pos, pend[0], pend[1], re0, re1);
-                    st_shared_v4(smem_u32(sX + (stage + 1) * XB) + pos, pend[2], pend[3], im0, im1);
+                    st_shared_v4(smem_u32(sX + stage * XB + SLAB) + pos, pend[2], pend[3], im0, im1);
                 }
                 if ((u & 15) == 15 || u == kU - 1) {
                     fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) {
-                        mbar_arrive_cluster(&full[stage], 0);
-                        mbar_arrive_cluster(&full[stage + 1], 0);
-                    }
-                    stage += 2;
-                    if (stage == NSTAGES) {
+                    if (lane == 0) mbar_arrive_cluster(&full[stage], 0);
+                    if (++stage == NSTAGES) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -527,14 +520,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     constexpr int kUnitsRaw = (BPC == 4) ? Mi * (Mi - 1) / 2 : (Mi * (Mi - 1) / 2 + 1) / 2;
     constexpr int kU = (kUnitsRaw + 7) / 8 * 8;
     constexpr bool kHalfPair = FOLD && (kU % 16 == 8);      // last slab pair of a chunk holds 8 units: 2 MMAs
+    // FOLD stages hold a slab pair (Re, Im of the same 16 units): one barrier round trip per 8 MMAs, same ring bytes
+    constexpr int kSt = FOLD ? STAGES2 / 2 : STAGES2;
+    constexpr int kSP = FOLD ? 2 : 1;                       // slabs per stage
+    constexpr int kAS = kSP * A2_BYTES, kBS = kSP * B2_BYTES;
 
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sA = smem;
-    uint8_t* sB = smem + STAGES2 * A2_BYTES;
-    uint64_t* full = reinterpret_cast<uint64_t*>(sB + STAGES2 * B2_BYTES);
-    uint64_t* empty = full + STAGES2;
-    uint64_t* tfull = empty + STAGES2;
+    uint8_t* sB = smem + kSt * kAS;
+    uint64_t* full = reinterpret_cast<uint64_t*>(sB + kSt * kBS);
+    uint64_t* empty = full + kSt;
+    uint64_t* tfull = empty + kSt;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -548,7 +545,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     const uint32_t idesc = umma_idesc_f16(256, (uint32_t)bn);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES2; ++s) {
+        for (int s = 0; s < kSt; ++s) {
             // leader: its TMA (expect_tx) + the producer warps of both CTAs (peer ones arrive remotely)
             mbar_init(&full[s], kProducer ? 1 + 2 * NPW2 : 1);
             mbar_init(&empty[s], 1);
@@ -574,16 +571,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            const uint32_t bytes = kProducer ? 2 * A2_BYTES : 2 * (A2_BYTES + B2_BYTES);
+            const uint32_t bytes = kSP * (kProducer ? 2 * A2_BYTES : 2 * (A2_BYTES + B2_BYTES));
             for (int t = pair; t < units; t += n_pairs) {
                 const Unit w = unit_of(p, t);
-                for (int ks = w.k0; ks < w.k1; ++ks) {
+                for (int ks = w.k0; ks < w.k1; ks += kSP) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
-                    tma_load_2d_2sm(sA + stage * A2_BYTES, &tmA, (p.dbg & 2) ? 0 : ks * BK, (p.dbg & 2) ? (int)rank * 128 : w.m * 256 + (int)rank * 128, &full[stage]);
-                    if (!kProducer)
-                        tma_load_2d_2sm(sB + stage * B2_BYTES, &tmB, ks * BK, w.n * bn + (int)rank * hb, &full[stage]);
-                    if (++stage == STAGES2) {
+#pragma unroll
+                    for (int j = 0; j < kSP; ++j) {
+                        tma_load_2d_2sm(sA + stage * kAS + j * A2_BYTES, &tmA, (p.dbg & 2) ? 0 : (ks + j) * BK,
+                                        (p.dbg & 2) ? (int)rank * 128 : w.m * 256 + (int)rank * 128, &full[stage]);
+                        if (!kProducer)
+                            tma_load_2d_2sm(sB + stage * kBS + j * B2_BYTES, &tmB, (ks + j) * BK,
+                                            w.n * bn + (int)rank * hb, &full[stage]);
+                    }
+                    if (++stage == kSt) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -604,23 +606,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                 const Unit w = unit_of(p, t);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                int local = 0;                                      // slab index within the bin chunk (FOLD)
-                for (int ks = w.k0; ks < w.k1; ++ks) {
+                int lp = 0;                                         // slab pair within the bin chunk (FOLD)
+                const int n_lp = p.spc / 2;
+                for (int ks = w.k0; ks < w.k1; ks += kSP) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint64_t ad = adesc0 + (uint64_t)(stage * (A2_BYTES >> 4));
-                    const uint64_t bd = bdesc0 + (uint64_t)(stage * (B2_BYTES >> 4));
+                    const uint64_t ad = adesc0 + (uint64_t)(stage * (kAS >> 4));
+                    const uint64_t bd = bdesc0 + (uint64_t)(stage * (kBS >> 4));
                     if constexpr (FOLD) {
-                        const uint32_t d_tmem = tmem_base + (uint32_t)(local & 1) * BN;   // Re -> a, Im -> b
-                        const bool half = kHalfPair && local >= p.spc - 2;
-                        const uint32_t acc0 = ks >= w.k0 + 2;
-                        umma_f16_2sm_warp(d_tmem, ad, bd, idesc, acc0);
-                        umma_f16_2sm_warp(d_tmem, ad + 2, bd + 2, idesc, 1u);
-                        if (!half) {
-                            umma_f16_2sm_warp(d_tmem, ad + 4, bd + 4, idesc, 1u);
-                            umma_f16_2sm_warp(d_tmem, ad + 6, bd + 6, idesc, 1u);
+                        const bool half = kHalfPair && lp == n_lp - 1;
+                        const uint32_t acc0 = ks != w.k0;
+#pragma unroll
+                        for (int part = 0; part < 2; ++part) {          // Re slab -> a, Im slab -> b
+                            const uint32_t d_tmem = tmem_base + (uint32_t)part * BN;
+                            const uint64_t pa = ad + part * (A2_BYTES >> 4), pb = bd + part * (B2_BYTES >> 4);
+                            umma_f16_2sm_warp(d_tmem, pa, pb, idesc, acc0);
+                            umma_f16_2sm_warp(d_tmem, pa + 2, pb + 2, idesc, 1u);
+                            if (!half) {
+                                umma_f16_2sm_warp(d_tmem, pa + 4, pb + 4, idesc, 1u);
+                                umma_f16_2sm_warp(d_tmem, pa + 6, pb + 6, idesc, 1u);
+                            }
                         }
-                        if (++local == p.spc) local = 0;
+                        if (++lp == n_lp) lp = 0;
                     } else {
                         const uint32_t d_tmem = tmem_base + acc * BN;
                         const uint32_t acc0 = ks != w.k0;
@@ -629,7 +636,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                             umma_f16_2sm_warp(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, kk ? 1u : acc0);
                     }
                     umma_commit_2sm_warp(&empty[stage], 0x3);
-                    if (++stage == STAGES2) {
+                    if (++stage == kSt) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -718,8 +725,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
             const Unit w = unit_of(p, t);
             const int f = w.n * bn + (int)rank * hb + tp;
             const bool valid = f < p.F && tp < hb && !(p.dbg & 1);
-            produce_x_pair<Mi, BPC, STAGES2, B2_BYTES, FOLD>(p, w, f, valid, sB, full, empty, stage, phase, row_off,
-                                                             xr);
+            produce_x_pair<Mi, BPC, kSt, kBS, FOLD, B2_BYTES>(p, w, f, valid, sB, full, empty, stage, phase, row_off,
+                                                              xr);
         }
     }
 
@@ -747,13 +754,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     constexpr int kUnitsRaw = (BPC == 4) ? Mi * (Mi - 1) / 2 : (Mi * (Mi - 1) / 2 + 1) / 2;
     constexpr int kU = (kUnitsRaw + 7) / 8 * 8;
     constexpr bool kHalfPair = FOLD && (kU % 16 == 8);
+    constexpr int kSt = FOLD ? STAGES2 / 2 : STAGES2;       // FOLD: a stage holds a (Re, Im) slab pair
+    constexpr int kSP = FOLD ? 2 : 1;
+    constexpr int kAS = kSP * A2_BYTES, kBS = kSP * B2_BYTES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sX = smem;                                     // A: 128 frames x 64 K per stage
-    uint8_t* sV = smem + STAGES2 * A2_BYTES;                // B: nt/2 V rows x 64 K per stage (<= 16 KB)
-    uint64_t* full = reinterpret_cast<uint64_t*>(sV + STAGES2 * B2_BYTES);
-    uint64_t* empty = full + STAGES2;
-    uint64_t* tfull = empty + STAGES2;
+    uint8_t* sX = smem;                                     // A: 128 frames x 64 K per slab
+    uint8_t* sV = smem + kSt * kAS;                         // B: nt/2 V rows x 64 K per slab (<= 16 KB)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sV + kSt * kBS);
+    uint64_t* empty = full + kSt;
+    uint64_t* tfull = empty + kSt;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -767,7 +777,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     const uint32_t idesc = umma_idesc_f16(256, (uint32_t)nt);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES2; ++s) {
+        for (int s = 0; s < kSt; ++s) {
             mbar_init(&full[s], 1 + 2 * NPW2);              // leader's TMA (expect_tx) + producers of both CTAs
             mbar_init(&empty[s], 1);
         }
@@ -789,14 +799,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            const uint32_t bytes = 2u * (uint32_t)hn * BK * 2;
+            const uint32_t bytes = kSP * 2u * (uint32_t)hn * BK * 2;
             for (int t = pair; t < units; t += n_pairs) {
                 const Unit w = unit_of_f(p, t);
-                for (int ks = w.k0; ks < w.k1; ++ks) {
+                for (int ks = w.k0; ks < w.k1; ks += kSP) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
-                    tma_load_2d_2sm(sV + stage * B2_BYTES, &tmV, ks * BK, w.n * nt + (int)rank * hn, &full[stage]);
-                    if (++stage == STAGES2) {
+#pragma unroll
+                    for (int j = 0; j < kSP; ++j)
+                        tma_load_2d_2sm(sV + stage * kBS + j * B2_BYTES, &tmV, (ks + j) * BK, w.n * nt + (int)rank * hn,
+                                        &full[stage]);
+                    if (++stage == kSt) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -814,22 +827,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                 const Unit w = unit_of_f(p, t);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                int local = 0;
-                for (int ks = w.k0; ks < w.k1; ++ks) {
+                int lp = 0;
+                const int n_lp = p.spc / 2;
+                for (int ks = w.k0; ks < w.k1; ks += kSP) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint64_t ad = adesc0 + (uint64_t)(stage * (A2_BYTES >> 4));
-                    const uint64_t bd = bdesc0 + (uint64_t)(stage * (B2_BYTES >> 4));
+                    const uint64_t ad = adesc0 + (uint64_t)(stage * (kAS >> 4));
+                    const uint64_t bd = bdesc0 + (uint64_t)(stage * (kBS >> 4));
                     if constexpr (FOLD) {
-                        const uint32_t d_tmem = tmem_base + (uint32_t)(local & 1) * BN;
-                        const bool half = kHalfPair && local >= p.spc - 2;
-                        umma_f16_2sm_warp(d_tmem, ad, bd, idesc, ks >= w.k0 + 2);
-                        umma_f16_2sm_warp(d_tmem, ad + 2, bd + 2, idesc, 1u);
-                        if (!half) {
-                            umma_f16_2sm_warp(d_tmem, ad + 4, bd + 4, idesc, 1u);
-                            umma_f16_2sm_warp(d_tmem, ad + 6, bd + 6, idesc, 1u);
+                        const bool half = kHalfPair && lp == n_lp - 1;
+                        const uint32_t acc0 = ks != w.k0;
+#pragma unroll
+                        for (int part = 0; part < 2; ++part) {          // Re slab -> a (Z_r), Im slab -> b (Z_i)
+                            const uint32_t d_tmem = tmem_base + (uint32_t)part * BN;
+                            const uint64_t pa = ad + part * (A2_BYTES >> 4), pb = bd + part * (B2_BYTES >> 4);
+                            umma_f16_2sm_warp(d_tmem, pa, pb, idesc, acc0);
+                            umma_f16_2sm_warp(d_tmem, pa + 2, pb + 2, idesc, 1u);
+                            if (!half) {
+                                umma_f16_2sm_warp(d_tmem, pa + 4, pb + 4, idesc, 1u);
+                                umma_f16_2sm_warp(d_tmem, pa + 6, pb + 6, idesc, 1u);
+                            }
                         }
-                        if (++local == p.spc) local = 0;
+                        if (++lp == n_lp) lp = 0;
                     } else {
                         const uint32_t d_tmem = tmem_base + acc * BN;
                         const uint32_t acc0 = ks != w.k0;
@@ -838,7 +857,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                             umma_f16_2sm_warp(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, kk ? 1u : acc0);
                     }
                     umma_commit_2sm_warp(&empty[stage], 0x3);
-                    if (++stage == STAGES2) {
+                    if (++stage == kSt) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -912,8 +931,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
         for (int t = pair; t < units; t += n_pairs) {
             const Unit w = unit_of_f(p, t);
             const int f = w.m * 256 + (int)rank * 128 + tp;
-            produce_x_pair<Mi, BPC, STAGES2, A2_BYTES, FOLD>(p, w, f, f < p.F, sX, full, empty, stage, phase,
-                                                             row_off, xr);
+            produce_x_pair<Mi, BPC, kSt, kAS, FOLD, A2_BYTES>(p, w, f, f < p.F, sX, full, empty, stage, phase,
+                                                              row_off, xr);
         }
     }
 

@@ -126,7 +126,7 @@ __device__ __forceinline__ int bitrev_r(int i) {
 // registers, twiddle, transpose through padded smem; pass 2: the 32-point DFTs over the lane index split as
 // R-point in registers x G = 32/R across lanes).  Then the real-FFT post pass, PHAT, FP16 records.
 template <int R, int BPC>
-__global__ void __launch_bounds__(32 * STFT_WARPS, R >= 32 ? 1 : 5)
+__global__ void __launch_bounds__(32 * STFT_WARPS)
     stft_phat_kernel(const float* __restrict__ audio, int64_t cs, int64_t fstride, int F, int Mi, int64_t F_pad,
                      const float* __restrict__ win, const float2* __restrict__ twN, uint8_t* __restrict__ P16,
                      int n_chunks, int k_lo, int k_hi, const uint8_t* __restrict__ mask, int64_t mask_stride) {
@@ -139,6 +139,8 @@ __global__ void __launch_bounds__(32 * STFT_WARPS, R >= 32 ? 1 : 5)
     constexpr int WBUF = (R * SROW > H + H / 16 + 2) ? R * SROW : H + H / 16 + 2;   // float2 per warp (even)
     extern __shared__ __align__(16) uint8_t sm[];
     float2* wbuf = reinterpret_cast<float2*>(sm) + (threadIdx.x >> 5) * WBUF;
+    const int tile_stride = STFT_WARPS * 16 + 16;                                    // padded chunk row (bytes)
+    uint8_t* tile = sm + STFT_WARPS * WBUF * sizeof(float2);                        // [n_chunks][tile_stride]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m = blockIdx.y;
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(32 * STFT_WARPS, R >= 32 ? 1 : 5)
 
     // ---- real-FFT post pass + PHAT: one lane per record (BPC consecutive bins), 2X = (Z_k + conj Z_{H-k}) -
     // j w^k (Z_k - conj Z_{H-k}) (the factor 1/2 is dropped: PHAT is scale-invariant and 2 is exact), one 16- or
-    // 8-byte global store per record.  Bin H (Nyquist) = Re Z_0 - Im Z_0 is the lone bin of the last record.
+    // 8-byte shared store per record.  Bin H (Nyquist) = Re Z_0 - Im Z_0 is the lone bin of the last record.
     {
         constexpr int NREC = H / BPC;                                   // records of bins 0..H-1
         const bool filter = (k_lo > 0) || (k_hi < Kb) || (mask != nullptr);
@@ -261,8 +263,7 @@ __global__ void __launch_bounds__(32 * STFT_WARPS, R >= 32 ? 1 : 5)
 #pragma unroll
                 for (int s2 = 0; s2 < BPC; ++s2) re[s2] = im[s2] = 0.f;
             }
-            // the record goes straight to P16[c][m][f]: the 8 warps of the CTA (frames f0..f0+7) fill the line together
-            uint8_t* rec = P16 + (((int64_t)c * Mi + m) * F_pad + f) * (BPC * 4);
+            uint8_t* rec = tile + c * tile_stride + warp * (BPC * 4);
             if constexpr (BPC == 4) {
                 const __half2 h0 = __floats2half2_rn(re[0], re[1]), h1 = __floats2half2_rn(re[2], re[3]);
                 const __half2 h2 = __floats2half2_rn(im[0], im[1]), h3 = __floats2half2_rn(im[2], im[3]);
@@ -276,23 +277,29 @@ __global__ void __launch_bounds__(32 * STFT_WARPS, R >= 32 ? 1 : 5)
                                                             *reinterpret_cast<const uint32_t*>(&h1));
             }
         }
-        if (lane == 0 && live) {                                        // record NREC: bin H, zero padding after it
+        if (lane == 0) {                                                // record NREC: bin H, zero padding after it
             float e = 0.f;
-            if (H >= k_lo && H < k_hi && (!mask || mask[(int64_t)f * mask_stride + H])) {
+            if (live && H >= k_lo && H < k_hi && (!mask || mask[(int64_t)f * mask_stride + H])) {
                 const float2 Z0 = wbuf[0];
                 const float v = Z0.x - Z0.y;
                 e = v > 0.f ? 1.f : (v < 0.f ? -1.f : 0.f);
             }
-            __half2 h[BPC];
-            h[0] = __floats2half2_rn(e, 0.f);
+            __half* rec = reinterpret_cast<__half*>(tile + NREC * tile_stride + warp * (BPC * 4));
 #pragma unroll
-            for (int q = 1; q < BPC; ++q) h[q] = __floats2half2_rn(0.f, 0.f);
-            uint8_t* rec = P16 + (((int64_t)NREC * Mi + m) * F_pad + f) * (BPC * 4);
-            if constexpr (BPC == 4)
-                *reinterpret_cast<uint4*>(rec) = *reinterpret_cast<const uint4*>(h);
-            else
-                *reinterpret_cast<uint2*>(rec) = *reinterpret_cast<const uint2*>(h);
+            for (int s2 = 0; s2 < 2 * BPC; ++s2) rec[s2] = __float2half_rn(0.f);
+            rec[0] = __float2half_rn(e);
         }
+    }
+    __syncthreads();
+
+    // ---- coalesced write-out: per chunk, 8 frames x unit_bytes contiguous at P16[c][m][f0..f0+7]
+    constexpr int unit_bytes = BPC * 4;
+    constexpr int vec_per_chunk = STFT_WARPS * unit_bytes / 16;      // 16-byte stores: 8 (bpc 4) or 4 (bpc 2)
+    const int total = n_chunks * vec_per_chunk;
+    for (int i = threadIdx.x; i < total; i += blockDim.x) {
+        const int cc = i / vec_per_chunk, wi = i % vec_per_chunk;
+        uint4* out = reinterpret_cast<uint4*>(P16 + (((int64_t)cc * Mi + m) * F_pad + f0) * unit_bytes);
+        out[wi] = reinterpret_cast<const uint4*>(tile + cc * tile_stride)[wi];
     }
 }
 
@@ -347,7 +354,7 @@ template <int R, int BPC>
 static cudaError_t launch_rb(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F, cudaStream_t s) {
     const int H = 32 * R;
     const int wbuf = (R * 34 > H + H / 16 + 2) ? R * 34 : H + H / 16 + 2;
-    const size_t smem = STFT_WARPS * wbuf * sizeof(float2);
+    const size_t smem = STFT_WARPS * wbuf * sizeof(float2) + (size_t)p.L.n_chunks * (STFT_WARPS * 16 + 16);
     dim3 grid((F + STFT_WARPS - 1) / STFT_WARPS, p.M);
     stft_phat_kernel<R, BPC><<<grid, 32 * STFT_WARPS, smem, s>>>(audio, cs, fstride, F, p.L.Mi, p.F_pad, p.d_window,
                                                                  p.d_twN, p.d_P16, p.L.n_chunks, p.k_lo, p.k_hi,
