@@ -686,3 +686,40 @@ def test_real_v_projection(M, planar, monkeypatch):
     PP.compare(res["1"][0][keep], res["1"][1][keep], P_, Y_at, f"M={M} real V")
     same = res["1"][0] == res["0"][0]
     assert same.mean() >= 0.99
+
+
+def test_srp_last_fold_row():
+    """The folded W of a 2562-point grid (no twins) has 1281 rows = 5 x 256 + 1: the last fold row sits alone in the
+    6th 256-row tile of the CTA-pair GEMM (rows past it are zero padding).  Sources placed exactly on that row's two
+    classes (a point and its antipode) must come back, and every frame must pass the oracle parity rules."""
+    from workloads import geometry as G
+    from workloads import scenes as SC
+    rng = np.random.default_rng(5150)
+    M, N, hop = 12, 256, 128
+    mics = rng.uniform(-0.07, 0.07, (M, 3))
+    pts = G.icosphere(4)
+    key = {r.tobytes(): i for i, r in enumerate(pts + 0.0)}
+    anti = np.array([key[((-r) + 0.0).tobytes()] for r in pts])
+    last = max(min(q, anti[q]) for q in range(len(pts)))            # the fold row built last (R22 pairing order)
+    targets = [last, anti[last]]
+    F = 64
+    frames = []
+    for f in range(F):
+        u = pts[targets[f % 2]]
+        frames.append(SC.plane_wave_stream(rng, mics, 16000.0, 343.0, N, u, 20.0))
+    audio = np.ascontiguousarray(np.stack(frames).astype(np.float32))            # framed [F][M][N]
+    # max_frames large enough that the plan has no small-batch split path: the argmax epilogue path runs
+    plan = S.Plan(mics, pts, 16000.0, 343.0, N, hop, "far", methods=("srp",), max_frames=4096)
+    assert plan.info()["srp_rows"] == 1281
+    d = torch.from_numpy(audio).to(DEV)
+    doa = torch.empty(F, dtype=torch.int32, device=DEV)
+    sc = torch.empty(F, dtype=torch.float32, device=DEV)
+    plan.localize("srp", d, F, N, M * N, doa, sc, torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    q, s = doa.cpu().numpy(), sc.cpu().numpy()
+    tau = srp.tdoa(mics, pts, 16000.0, 343.0, "far")
+    x = srp.frames_to_x(audio.astype(np.float64))
+    P_, Y_at = PP.srp_reference(tau, x, N)
+    PP.compare(q, s, P_, Y_at, "tail rows")
+    assert np.mean(q == np.array([targets[f % 2] for f in range(F)])) >= 0.95
+    plan.close()
