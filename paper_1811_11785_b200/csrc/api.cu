@@ -143,6 +143,7 @@ struct svdphat_plan_s {
         if (p.svd_stream) cudaStreamDestroy(p.svd_stream);
         if (p.srp_stream) cudaStreamDestroy(p.srp_stream);
         if (p.ev_join2) cudaEventDestroy(p.ev_join2);
+        if (p.ev_z) cudaEventDestroy(p.ev_z);
         void* bufs[] = {p.d_W16,   p.d_V16,   p.d_R16,   p.d_rep,   p.d_delay,     p.d_window,      p.d_twN,
                         p.d_P16,   p.d_keys,  p.d_Z32,   p.d_Zs16,  p.d_zflag,     p.d_stage,       p.d_doa_stage,
                         p.d_score_stage, p.d_S, p.d_cls, p.d_dirs, p.d_Ypart, p.d_fold_cls};
@@ -433,6 +434,15 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     if (p.methods & SVDPHAT_METHOD_SVD) {
         st = setup_svd_operands(p, d_tau, d->rank_D);
         if (st != SVDPHAT_OK) return st;
+        // SRP fold rows past the last full 256-row tile ride in the projection's spare V rows (BOTH calls)
+        const int nr = p.fold_rows % 256;
+        if (p.fold && p.svd_fold && p.pair_proj && p.fold_rows > 256 && nr > 0 && nr <= 8 && p.D + nr <= p.V_rows &&
+            p.D + nr <= p.Dh && 2 * p.Dh <= 4096 && p.K_W == p.K_F) {
+            p.tail_r0 = p.fold_rows - nr;
+            p.tail_n = nr;
+            SVD_CUDA_TRY(cudaMemcpy(p.d_V16 + (int64_t)p.D * p.K_F, p.d_W16 + (int64_t)p.tail_r0 * p.K_W,
+                                    (size_t)nr * p.K_F * sizeof(__half), cudaMemcpyDeviceToDevice));
+        }
         if (!encode_2d(&p.tm_V, p.d_V16, p.V_rows, p.svd_fold ? p.K_F : p.L.K_total,
                        p.pair_proj ? p.proj_nt / 2 : 128))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(V) failed");
@@ -486,6 +496,7 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
         SVD_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming));
         SVD_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming));
         SVD_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_join2, cudaEventDisableTiming));
+        SVD_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_z, cudaEventDisableTiming));
     }
     SVD_CUDA_TRY(cudaDeviceSynchronize());
     p.setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
@@ -547,16 +558,25 @@ static svdphat_status localize_impl(Plan& p, int32_t method, const float* d_audi
     }
     int32_t* const doas[2] = {doa_srp, doa_svd};
     float* const scores[2] = {sc_srp, sc_svd};
-    if (method & SVDPHAT_METHOD_SRP) {
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_GEMM, sr, [&] { return launch_gemm(p, 0, F, sr); }));
-        // forked: the SRP half of the finalize runs on the SRP stream while the SVD chain is still busy
-        if (fork)
-            SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_FINALIZE, sr,
-                                [&] { return launch_finalize(p, SVDPHAT_METHOD_SRP, F, doas, scores, sr); }));
-    }
+    // SRP tail rows scored through the projection: BOTH calls on the argmax GEMM path (not the small-batch split)
+    const bool both = method == SVDPHAT_METHOD_BOTH && p.tail_n > 0 && srp_split_ways(p, F) == 1;
+    if (method & SVDPHAT_METHOD_SRP)
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_GEMM, sr, [&] { return launch_gemm(p, 0, F, sr, both); }));
     if (method & SVDPHAT_METHOD_SVD) {
         SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_PROJ, sv, [&] { return launch_gemm(p, 1, F, sv); }));
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_NORM, sv, [&] { return launch_zsplit(p, F, sv); }));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_NORM, sv, [&] { return launch_zsplit(p, F, sv, both); }));
+    }
+    // forked: the SRP half of the finalize runs on the SRP stream while the SVD search is still busy (after zsplit
+    // when the SRP tail rows' keys come from it)
+    if (fork && (method & SVDPHAT_METHOD_SRP)) {
+        if (both) {
+            SVD_CUDA_TRY(cudaEventRecord(p.ev_z, sv));
+            SVD_CUDA_TRY(cudaStreamWaitEvent(sr, p.ev_z, 0));
+        }
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_FINALIZE, sr,
+                            [&] { return launch_finalize(p, SVDPHAT_METHOD_SRP, F, doas, scores, sr); }));
+    }
+    if (method & SVDPHAT_METHOD_SVD) {
         SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_SEARCH, sv, [&] { return launch_gemm(p, 2, F, sv); }));
         if (fork)
             SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_FINALIZE, sv,

@@ -59,11 +59,21 @@ __global__ void zsplit_kernel(float* __restrict__ Z, int F, int64_t F_pad, int l
 // The same, one 128-thread CTA per frame with the frame's Z held in registers (NV float4 per thread, ldz <= 512 NV):
 // every partial is read once with 16-byte loads, all NV x nsplit loads of a thread in flight together.
 constexpr int ZS_THREADS = 128;
+// Tail (fold + real V, Plan::tail_n): columns D + r (a) and D_h + D + r (b), r < tail_n, hold the SRP fold row
+// tail_r0 + r.  They always leave Z (zeroed before the norm); for a BOTH call (keys != nullptr) they are scored
+// Y_c = a - b, Y_c' = a + b into the SRP keys.
+struct ZTail {
+    int n, D, r0, fold_rows;
+    const int* fold_cls;
+    unsigned long long* keys;
+};
+
 template <int NV>
 __global__ void __launch_bounds__(ZS_THREADS)
     zsplit_cta_kernel(float* __restrict__ Z, int64_t F_pad, int ldz, int nsplit, __half* __restrict__ Zs, int K2,
-                      int* __restrict__ zflag) {
+                      int* __restrict__ zflag, ZTail tail) {
     __shared__ float s_ss[ZS_THREADS / 32];
+    __shared__ float s_tail[2][8];
     const int f = blockIdx.x;
     const int t = threadIdx.x;
     const int n4 = ldz >> 2;
@@ -90,6 +100,25 @@ __global__ void __launch_bounds__(ZS_THREADS)
             v[j].w += w[j].w;
         }
     }
+    if (tail.n > 0) {
+        const int half = ldz >> 1;
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            const int i = t + ZS_THREADS * j;
+            if (i < n4) {
+                float* e = reinterpret_cast<float*>(&v[j]);
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const int col = 4 * i + q;
+                    const int r = col < half ? col - tail.D : col - half - tail.D;
+                    if (r >= 0 && r < tail.n) {
+                        s_tail[col < half ? 0 : 1][r] = e[q];
+                        e[q] = 0.f;
+                    }
+                }
+            }
+        }
+    }
     float ss = 0.f;
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
@@ -107,7 +136,21 @@ __global__ void __launch_bounds__(ZS_THREADS)
 #pragma unroll
     for (int w = 0; w < ZS_THREADS / 32; ++w) ss += s_ss[w];   // same order in every thread
     const float inv = ss > 0.f ? rsqrtf(ss) : 0.f;
-    if (t == 0) zflag[f] = ss > 0.f ? 0 : 1;
+    if (t == 0) {
+        zflag[f] = ss > 0.f ? 0 : 1;
+        unsigned long long best = 0ull;
+        for (int r = 0; tail.keys && r < tail.n; ++r) {
+            const float a = s_tail[0][r], b = s_tail[1][r];
+            const int cm = tail.fold_cls[tail.r0 + r], cp = tail.fold_cls[tail.fold_rows + tail.r0 + r];
+            const float ym = a - b, yp = a + b;
+            const unsigned long long km = ym == ym ? ((unsigned long long)f2o_dev(ym) << 32) | (0xFFFFFFFFull - cm) : 0ull;
+            const unsigned long long kp =
+                (cp >= 0 && yp == yp) ? ((unsigned long long)f2o_dev(yp) << 32) | (0xFFFFFFFFull - cp) : 0ull;
+            best = km > best ? km : best;
+            best = kp > best ? kp : best;
+        }
+        if (best) atomicMax(&tail.keys[f], best);
+    }
     uint2* out = reinterpret_cast<uint2*>(Zs + (int64_t)f * K2);     // 4 halves per store
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
@@ -291,19 +334,21 @@ cudaError_t launch_split_argmax(const Plan& p, int F, int S, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s) {
+cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s, bool both) {
     if (F <= 0) return cudaSuccess;
     const int ldz = 2 * p.Dh, S = proj_shape(p, F).ksplit;
     if (ldz % 4 == 0 && ldz <= 4 * ZS_THREADS * 8) {
         const int nv = (ldz / 4 + ZS_THREADS - 1) / ZS_THREADS;
+        // the tail columns always leave Z; their keys are only wanted by a BOTH call (the SRP GEMM then skips them)
+        const ZTail tl{p.tail_n, p.D, p.tail_r0, p.fold_rows, p.d_fold_cls, both ? p.d_keys : nullptr};
         if (nv <= 1)
-            zsplit_cta_kernel<1><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag);
+            zsplit_cta_kernel<1><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag, tl);
         else if (nv <= 2)
-            zsplit_cta_kernel<2><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag);
+            zsplit_cta_kernel<2><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag, tl);
         else if (nv <= 4)
-            zsplit_cta_kernel<4><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag);
+            zsplit_cta_kernel<4><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag, tl);
         else
-            zsplit_cta_kernel<8><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag);
+            zsplit_cta_kernel<8><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag, tl);
         return cudaGetLastError();
     }
     const int threads = 256;

@@ -1278,7 +1278,18 @@ void set_band(Plan& p, int k_lo, int k_hi, const uint8_t* mask, int64_t mask_str
     p.mask_stride = mask_stride;
 }
 
-cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
+// K splits of the small-batch SRP path (fewer 256 x 256 units than half the CTA pairs), 1 = the argmax GEMM path
+int srp_split_ways(const Plan& p, int F) {
+    if (!p.pair_srp || p.srp_split_max <= 1) return 1;
+    const int npairs = p.num_sms / 2;
+    const int units = (p.W_rows / 256) * ((F + 255) / 256);
+    int S = units > 0 ? npairs / units : 1;
+    S = S < p.srp_split_max ? S : p.srp_split_max;
+    S = S < p.c_hi - p.c_lo ? S : p.c_hi - p.c_lo;
+    return (units * 2 <= npairs && S > 1) ? S : 1;
+}
+
+cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s, bool both) {
     GemmParams gp{};
     const bool srp_mode = (mode == 0 || mode == 3);             // W16 operand (folded when p.fold)
     const bool producer_mode = srp_mode || mode == 1;
@@ -1404,23 +1415,21 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s) {
 #undef SVD_DISPATCH3
         return cudaErrorInvalidValue;
     }
-    if (mode == 0 && p.pair_srp && p.srp_split_max > 1) {
+    if (mode == 0 && srp_split_ways(p, F) > 1) {
         // small batch: fewer units than half the CTA pairs -> split K into chunk ranges with partial power maps
+        const int S = srp_split_ways(p, F);
         const int units = gp.m_tiles * gp.n_tiles;
-        int S = units > 0 ? npairs / units : 1;
-        S = S < p.srp_split_max ? S : p.srp_split_max;
-        S = S < p.c_hi - p.c_lo ? S : p.c_hi - p.c_lo;
-        if (units * 2 <= npairs && S > 1) {
-            gp.ksplit = S;
-            gp.Z = p.d_Ypart;
-            gp.ldz = p.Q_pad;
-            const cudaError_t e = launch_pair<1>(p, *A, *B, gp, units * S < npairs ? units * S : npairs, p.fold, s);
-            return e != cudaSuccess ? e : launch_split_argmax(p, F, S, s);
-        }
+        gp.ksplit = S;
+        gp.Z = p.d_Ypart;
+        gp.ldz = p.Q_pad;
+        const cudaError_t e = launch_pair<1>(p, *A, *B, gp, units * S < npairs ? units * S : npairs, p.fold, s);
+        return e != cudaSuccess ? e : launch_split_argmax(p, F, S, s);
     }
     if (mode == 0 && p.pair_srp) {
         gp.bn = fixed_bn ? fixed_bn : 256;
         gp.n_tiles = (F + gp.bn - 1) / gp.bn;
+        if (both && p.tail_n > 0) gp.m_tiles = p.tail_r0 / 256;   // the tail rows are scored by the projection
+        // (a BOTH call reaches here only on the argmax path: srp_split_ways(p, F) == 1, see localize_impl)
         const int units = gp.m_tiles * gp.n_tiles;
         return launch_pair<0>(p, *A, *B, gp, units < npairs ? units : npairs, p.fold, s);
     }

@@ -61,6 +61,10 @@ struct Plan {
     // SVD is taken of the real W~ = T W (rows sqrt2 Re W_c, sqrt2 Im W_c per pair, W_c for a real row), so V is real
     // and Z_r = V^T x_r, Z_i = V^T x_i: the projection runs as a fold GEMM on D rows (a -> Z_r, b -> Z_i).
     bool svd_fold = false;
+    // BOTH with fold + real V: the few fold rows past the last full 256-row SRP tile ride in spare rows [D, D+tail_n)
+    // of the projection's last V tile (W values copied there); zsplit turns their (a, b) into SRP keys, so the SRP
+    // GEMM skips that tile (cfg3/cfg4: 5121 = 20 x 256 + 1 rows -> one wave fewer).
+    int tail_r0 = -1, tail_n = 0;
     std::vector<int> rb_cls, rb_partner, rb_kind;   // real basis row i: class, antipode (-1), kind 0 Re / 1 Im / 2 real
     int64_t K_W = 0;              // contraction length of W16
     int spc_W = 0;                // W16 slabs per bin chunk
@@ -106,7 +110,7 @@ struct Plan {
     // kernels fill the SMs released by the SRP GEMM's last (partial) wave
     cudaStream_t svd_stream = nullptr;   // lowest priority
     cudaStream_t srp_stream = nullptr;   // highest priority: its CTAs are dispatched before the SVD chain's
-    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr;
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_join2 = nullptr, ev_z = nullptr;
     int32_t* d_doa_stage = nullptr;
     float* d_score_stage = nullptr;
     int64_t last_frames = 0;
@@ -150,8 +154,10 @@ cudaError_t launch_stft_phat(const Plan& p, const float* audio, int64_t cs, int6
                              cudaStream_t s);
 // mode: 0 = SRP argmax (A = W16, B = producer), 1 = SVD GEMM1 store Z (A = V16, B = producer),
 //       2 = SVD search argmax (A = R16, B = Zs16 via TMA), 3 = SRP power map -> d_S, 4 = SVD search power map -> d_S
-cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s);
-cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s);
+// both: a localize(BOTH) call, where the SRP tail rows travel through the projection (Plan::tail_n)
+cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s, bool both = false);
+cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s, bool both = false);
+int srp_split_ways(const Plan& p, int F);     // > 1: the SRP call takes the small-batch split-K path
 cudaError_t launch_split_argmax(const Plan& p, int F, int S, cudaStream_t s);
 constexpr int MAX_KSPLIT = 32;               // cap on K splits (chunk ranges) of the store-mode GEMMs
 struct ProjShape {

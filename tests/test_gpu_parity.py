@@ -723,3 +723,47 @@ def test_srp_last_fold_row():
     PP.compare(q, s, P_, Y_at, "tail rows")
     assert np.mean(q == np.array([targets[f % 2] for f in range(F)])) >= 0.95
     plan.close()
+
+
+def test_srp_last_fold_row_both():
+    """localize(BOTH) on a plan whose last SRP fold row is alone in its tile: with a real V the row rides in a
+    spare row of the SVD projection (Plan::tail_n) and its keys come from the Z normalisation; the SRP results must
+    match the SRP-only call (same plan), find sources placed on that row's classes, and the SVD results must pass
+    the oracle's SVD-PHAT parity."""
+    from workloads import geometry as G
+    from workloads import scenes as SC
+    rng = np.random.default_rng(5151)
+    M, N, hop = 12, 256, 128
+    mics = rng.uniform(-0.07, 0.07, (M, 3))
+    pts = G.icosphere(4)
+    key = {r.tobytes(): i for i, r in enumerate(pts + 0.0)}
+    anti = np.array([key[((-r) + 0.0).tobytes()] for r in pts])
+    last = max(min(q, anti[q]) for q in range(len(pts)))
+    targets = [last, anti[last]]
+    F = 64
+    audio = np.ascontiguousarray(np.stack(
+        [SC.plane_wave_stream(rng, mics, 16000.0, 343.0, N, pts[targets[f % 2]], 20.0) for f in range(F)]
+    ).astype(np.float32))
+    plan = S.Plan(mics, pts, 16000.0, 343.0, N, hop, "far", methods=("srp", "svd"), max_frames=4096)
+    inf = plan.info()
+    assert inf["srp_rows"] == 1281 and inf["svd_rows"] == inf["D"]
+    d = torch.from_numpy(audio).to(DEV)
+    st = torch.cuda.current_stream().cuda_stream
+    q2 = torch.empty(2 * F, dtype=torch.int32, device=DEV)
+    s2 = torch.empty(2 * F, dtype=torch.float32, device=DEV)
+    plan.localize("both", d, F, N, M * N, q2, s2, st)
+    q1 = torch.empty(F, dtype=torch.int32, device=DEV)
+    s1 = torch.empty(F, dtype=torch.float32, device=DEV)
+    plan.localize("srp", d, F, N, M * N, q1, s1, st)
+    torch.cuda.synchronize()
+    qb, sb = q2.cpu().numpy(), s2.cpu().numpy()
+    tau = srp.tdoa(mics, pts, 16000.0, 343.0, "far")
+    x = srp.frames_to_x(audio.astype(np.float64))
+    P_, Y_at = PP.srp_reference(tau, x, N)
+    PP.compare(qb[:F], sb[:F], P_, Y_at, "BOTH: SRP")
+    assert np.mean(qb[:F] == q1.cpu().numpy()) >= 0.98
+    assert np.mean(qb[:F] == np.array([targets[f % 2] for f in range(F)])) >= 0.95
+    fac = svd.svd_factors(tau, N, 1e-5)
+    P2, Y2 = PP.svd_reference(fac, tau, x, N)
+    PP.compare(qb[F:], sb[F:], P2, Y2, "BOTH: SVD")
+    plan.close()
