@@ -433,6 +433,14 @@ __device__ __forceinline__ void produce_x_pair(const GemmParams& p, const Unit& 
                 e[m][1] = v.y;
             }
         }
+        // L2 prefetch of the next chunk's records: the chunk-boundary reload then hits L2 (with N = 160 V rows the
+        // 3-deep ring of slab pairs holds ~2k MMA cycles, less than an HBM round trip)
+        if (p.prefetch && valid && c + 1 < w.c1) {
+            const uint8_t* nsrc = src + (int64_t)Mi * p.F_pad * kUB;
+#pragma unroll
+            for (int m = 0; m < Mi; ++m)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(nsrc + (int64_t)m * p.F_pad * kUB));
+        }
         uint32_t outw[4], pend[4];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
