@@ -766,4 +766,17 @@ def test_srp_last_fold_row_both():
     fac = svd.svd_factors(tau, N, 1e-5)
     P2, Y2 = PP.svd_reference(fac, tau, x, N)
     PP.compare(qb[F:], sb[F:], P2, Y2, "BOTH: SVD")
+    # the same BOTH call (fork, tail event, joins) captured as a CUDA graph and replayed: bitwise the eager result
+    gs = torch.cuda.Stream()
+    with torch.cuda.stream(gs):
+        plan.localize("both", d, F, N, M * N, q2, s2, gs.cuda_stream)
+    torch.cuda.synchronize()
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g, stream=gs):
+        plan.localize("both", d, F, N, M * N, q2, s2, gs.cuda_stream)
+    q2.fill_(-7)
+    g.replay()
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(q2.cpu().numpy(), qb)
+    np.testing.assert_array_equal(s2.cpu().numpy(), sb)
     plan.close()
