@@ -491,8 +491,14 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     if ((p.methods & SVDPHAT_METHOD_BOTH) == SVDPHAT_METHOD_BOTH) {
         int lo = 0, hi = 0;
         SVD_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        SVD_CUDA_TRY(cudaStreamCreateWithPriority(&p.svd_stream, cudaStreamNonBlocking, lo));
-        SVD_CUDA_TRY(cudaStreamCreateWithPriority(&p.srp_stream, cudaStreamNonBlocking, hi));
+        // which chain gets the SMs first after the STFT (SVDPHAT_SVD_FIRST=1: the short SVD projection, then the SRP
+        // GEMM; default: the SRP GEMM, the SVD chain filling its last wave)
+        static const bool svd_first = [] {
+            const char* e = getenv("SVDPHAT_SVD_FIRST");
+            return e && atoi(e) != 0;
+        }();
+        SVD_CUDA_TRY(cudaStreamCreateWithPriority(&p.svd_stream, cudaStreamNonBlocking, svd_first ? hi : lo));
+        SVD_CUDA_TRY(cudaStreamCreateWithPriority(&p.srp_stream, cudaStreamNonBlocking, svd_first ? lo : hi));
         SVD_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming));
         SVD_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming));
         SVD_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_join2, cudaEventDisableTiming));
