@@ -186,7 +186,10 @@ enum {
     SVDPHAT_DUMP_PHASORS = 1,  /* FP16 unit phasors of the last call, decoded to float32 [F][M][K_bins][2]     */
     SVDPHAT_DUMP_Z = 2,        /* float32 Z of the last SVD call [F][2*D] (Re then Im), scaled by sqrt(PK)       */
     SVDPHAT_DUMP_CLASS_REP = 3,/* int32 [Q_classes]: representative (lowest) point index of each steering class */
-    SVDPHAT_DUMP_KEYS = 4      /* uint64 [F]: packed (score, class) argmax keys of the last call                 */
+    SVDPHAT_DUMP_KEYS = 4,     /* uint64 [F]: packed (score, class) argmax keys of the last call                 */
+    SVDPHAT_DUMP_POWER = 5     /* float32 [F][Q_classes]: the power map of the last svdphat_localize_topk call -
+                                  SRP: Y_q of eq. 9 per steering class; SVD: Re{D^_q Z^} of eq. 14 - the raw GEMM
+                                  outputs, for element-wise parity                                               */
 };
 svdphat_status svdphat_debug_dump(svdphat_plan_t plan, int32_t what, int64_t n_frames, void* host_out,
                                   int64_t bytes);

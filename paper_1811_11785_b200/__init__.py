@@ -3,5 +3,6 @@
 The product is libsvdphat.so (C-ABI in include/svdphat.h, CUDA kernels for sm_100a in csrc/); this package is its
 thin Python binding.  Importing it loads the shared library and fails loudly if it is missing.
 """
-from ._lib import (DUMP_CLASS_REP, DUMP_KEYS, DUMP_PHASORS, DUMP_Z, LIB_PATH, Plan, SvdPhatError,  # noqa: F401
+from ._lib import (DUMP_CLASS_REP, DUMP_KEYS, DUMP_PHASORS, DUMP_POWER, DUMP_Z, LIB_PATH, Plan,  # noqa: F401
+                   SvdPhatError,
                    frame_count, lib)

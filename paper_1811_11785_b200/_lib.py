@@ -17,7 +17,7 @@ FIELD_FAR, FIELD_NEAR = 0, 1
 METHOD_SRP, METHOD_SVD, METHOD_BOTH = 1, 2, 3
 STAGES = {1: "stft_phat", 2: "srp_gemm", 3: "svd_proj", 4: "svd_norm", 5: "svd_search", 6: "finalize"}
 _METHOD = {"srp": METHOD_SRP, "svd": METHOD_SVD, "both": METHOD_BOTH}
-DUMP_PHASORS, DUMP_Z, DUMP_CLASS_REP, DUMP_KEYS = 1, 2, 3, 4
+DUMP_PHASORS, DUMP_Z, DUMP_CLASS_REP, DUMP_KEYS, DUMP_POWER = 1, 2, 3, 4, 5
 
 
 class PlanDesc(C.Structure):
@@ -184,6 +184,8 @@ class Plan:
             out = np.zeros((n_frames, 2 * inf["D"]), dtype=np.float32)
         elif what == DUMP_CLASS_REP:
             out = np.zeros(inf["Q_classes"], dtype=np.int32)
+        elif what == DUMP_POWER:
+            out = np.zeros((n_frames, inf["Q_classes"]), dtype=np.float32)
         else:
             out = np.zeros(n_frames, dtype=np.uint64)
         _check(lib.svdphat_debug_dump(self._h, what, n_frames, out.ctypes.data, out.nbytes), "debug_dump")

@@ -870,6 +870,13 @@ svdphat_status svdphat_debug_dump(svdphat_plan_t plan, int32_t what, int64_t n_f
                                 (size_t)F * 8, cudaMemcpyDeviceToHost));
         return SVDPHAT_OK;
     }
+    if (what == SVDPHAT_DUMP_POWER) {
+        if (!p.d_S) return fail(SVDPHAT_INVALID_ARG, "no svdphat_localize_topk call yet");
+        if (bytes < (int64_t)F * p.Q_eff * 4) return fail(SVDPHAT_INVALID_ARG, "buffer too small");
+        SVD_CUDA_TRY(cudaMemcpy2D(host_out, (size_t)p.Q_eff * 4, p.d_S, (size_t)p.Q_pad * 4, (size_t)p.Q_eff * 4, F,
+                                  cudaMemcpyDeviceToHost));
+        return SVDPHAT_OK;
+    }
     if (what == SVDPHAT_DUMP_Z) {
         if (!p.d_Z32) return fail(SVDPHAT_INVALID_ARG, "SVD not planned");
         if (bytes < (int64_t)F * 2 * p.D * 4) return fail(SVDPHAT_INVALID_ARG, "buffer too small");

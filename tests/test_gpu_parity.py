@@ -780,3 +780,61 @@ def test_srp_last_fold_row_both():
     np.testing.assert_array_equal(q2.cpu().numpy(), qb)
     np.testing.assert_array_equal(s2.cpu().numpy(), sb)
     plan.close()
+
+
+def _class_index(tau, rep):
+    """Steering class of every point: the class whose representative row equals the point's tau row bitwise."""
+    key = {tau[r].tobytes(): c for c, r in enumerate(rep)}
+    return np.array([key[(t + 0.0).tobytes()] for t in tau])
+
+
+@pytest.mark.parametrize("cfg", [1, 5, "3d"])
+def test_power_maps_elementwise(cfg):
+    """The raw GEMM outputs, element by element: the SRP power map Y_q (eq. 9; folded rows a -/+ b on
+    symmetric grids) and the SVD search scores Re{D^_q Z^} (eq. 14) of every steering class, per frame within
+    2e-3 of the frame's peak against the float64 oracle.  cfg1: planar (twins, fold, real V with self-antipodal
+    rows); '3d': random 3-D array on an icosphere (fold, real V); cfg5: near field (no fold, complex V)."""
+    from workloads import geometry as G
+    from workloads import scenes as SC
+    if cfg == "3d":
+        rng = np.random.default_rng(31)
+        mics = rng.uniform(-0.07, 0.07, (9, 3))
+        pts = G.icosphere(3)
+        N, hop, F = 256, 128, 40
+        L = (F - 1) * hop + N
+        audio = SC.plane_wave_stream(rng, mics, 16000.0, 343.0, L, pts[5], 5.0).astype(np.float32)
+        fs, c, field, cs, fst = 16000.0, 343.0, "far", L, hop
+    else:
+        w = make(cfg, 40)
+        mics, pts, N, F = w.mics, w.points, w.N, 40
+        audio, fs, c, field, cs, fst = w.audio, w.fs, w.c, w.field, w.channel_stride, w.frame_stride
+    plan = S.Plan(mics, pts, fs, c, N, N // 2, field, delta=1e-5, methods=("srp", "svd"), max_frames=F)
+    d = torch.from_numpy(np.ascontiguousarray(audio)).to(DEV)
+    dk = torch.empty(F, dtype=torch.int32, device=DEV)
+    sk = torch.empty(F, dtype=torch.float32, device=DEV)
+    st = torch.cuda.current_stream().cuda_stream
+    tau = srp.tdoa(mics, pts, fs, c, field)
+    fr = srp.extract_frames(audio, F, mics.shape[0], N, cs, fst)
+    x = srp.frames_to_x(fr)
+    rep = plan.debug_dump(S.DUMP_CLASS_REP, 0)
+    assert np.array_equal(_class_index(tau, rep)[rep], np.arange(len(rep)))
+    live = ~srp.degenerate(x)
+    # SRP
+    plan.localize_topk("srp", d, F, cs, fst, 1, 10.0, dk, sk, st)
+    torch.cuda.synchronize()
+    Yg = plan.debug_dump(S.DUMP_POWER, F)
+    Y = srp.srp_energy(tau, x, N)[:, rep]
+    err = np.max(np.abs(Yg - Y), axis=1) / np.max(np.abs(Y), axis=1).clip(1e-30)
+    assert np.all(err[live] <= 2e-3), err.max()
+    # SVD
+    plan.localize_topk("svd", d, F, cs, fst, 1, 10.0, dk, sk, st)
+    torch.cuda.synchronize()
+    Sg = plan.debug_dump(S.DUMP_POWER, F)
+    fac = svd.svd_factors(tau, N, 1e-5)
+    assert fac["D"] == plan.info()["D"]
+    Z = svd.project(fac["V"], x)
+    nz = np.linalg.norm(Z, axis=1, keepdims=True)
+    Sref = svd.search_scores(fac["Rhat"], Z / np.where(nz > 0, nz, 1.0))[:, rep]
+    err = np.max(np.abs(Sg - Sref), axis=1) / np.max(np.abs(Sref), axis=1).clip(1e-30)
+    assert np.all(err[live] <= 2e-3), err.max()
+    plan.close()
