@@ -102,15 +102,9 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16(uint32_t M, uint32_t N) {
            | ((M >> 4) << 24);  // [24,29) M >> 4
 }
 
-__device__ __forceinline__ void umma_f16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                         uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-// Warp-converged form (see umma_f16_2sm_warp).
+// One tcgen05.mma (cta_group::1), issued by the converged warp: every lane executes the asm with identical operands
+// and elect.sync picks the issuing lane, so ptxas keeps the operands in uniform registers (a single-thread issue
+// under `if (lane == 0)` costs an ELECT / R2UR.BROADCAST / BRA.U.ANY sequence per MMA).
 __device__ __forceinline__ void umma_f16_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                               uint32_t accumulate) {
     asm volatile(
@@ -119,16 +113,12 @@ __device__ __forceinline__ void umma_f16_warp(uint32_t tmem_d, uint64_t adesc, u
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Arrive (once) on an mbarrier when all previously issued tcgen05.mma of the warp have completed.
 __device__ __forceinline__ void umma_commit_warp(uint64_t* bar) {
     asm volatile(
         "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
         : "memory");
-}
-// Arrive (once) on an mbarrier when all previously issued tcgen05.mma of this thread have completed.
-__device__ __forceinline__ void umma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
-                 : "memory");
 }
 
 // TMEM -> registers: 32 lanes x 32 consecutive 32-bit columns (thread t of the warp gets lane base+t).
@@ -195,16 +185,7 @@ template <uint32_t kCols>
 __device__ __forceinline__ void tmem_dealloc_2sm(uint32_t taddr) {
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(taddr), "n"(kCols) : "memory");
 }
-__device__ __forceinline__ void umma_f16_2sm(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
-                                             uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-        : "memory");
-}
-// Warp-converged forms: every lane executes the asm with identical operands and elect.sync picks the issuing lane, so
-// ptxas can keep the operands in uniform registers (no per-MMA ELECT / R2UR.BROADCAST / BRA.U.ANY sequence).
+// CTA-pair MMA / commit from the converged warp (see umma_f16_warp); the leader CTA issues for both.
 __device__ __forceinline__ void umma_f16_2sm_warp(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
                                                   uint32_t accumulate) {
     asm volatile(
@@ -251,26 +232,7 @@ __device__ __forceinline__ void umma_commit_2sm(uint64_t* bar, uint16_t mask) {
         : "memory");
 }
 
-// ------------------------------------------------------------------------------------------------ loads
-// Volatile read-only vector loads: the compiler may not sink them to their first use (used to prefetch a whole
-// chunk of phasor records into registers one chunk ahead).
-__device__ __forceinline__ uint4 ldg_nc_v4_early(const void* p) {
-    uint4 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w)
-                 : "l"(p));
-    return r;
-}
-__device__ __forceinline__ uint2 ldg_nc_v2_early(const void* p) {
-    uint2 r;
-    asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];" : "=r"(r.x), "=r"(r.y) : "l"(p));
-    return r;
-}
-
 // ------------------------------------------------------------------------------------------------ misc
-__device__ __forceinline__ void st_shared_v2(uint32_t addr, uint32_t a, uint32_t b) {
-    asm volatile("st.shared.v2.b32 [%0], {%1, %2};" ::"r"(addr), "r"(a), "r"(b) : "memory");
-}
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
     asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(a), "r"(b), "r"(c), "r"(d)
                  : "memory");
