@@ -97,12 +97,15 @@ template <int Mi>
 struct PairTab {
     int i[Mi * (Mi - 1) / 2 + 1];
     int j[Mi * (Mi - 1) / 2 + 1];
-    constexpr PairTab() : i(), j() {
+    int last[Mi];                          // last pair index that uses mic m (its record is dead after it)
+    constexpr PairTab() : i(), j(), last() {
         int p = 0;
         for (int a = 0; a < Mi; ++a)
             for (int b = a + 1; b < Mi; ++b) {
                 i[p] = a;
                 j[p] = b;
+                last[a] = p;
+                last[b] = p;
                 ++p;
             }
     }
@@ -413,24 +416,39 @@ __device__ __forceinline__ void produce_x_pair(const GemmParams& p, const Unit& 
     constexpr int kU = (kUnitsRaw + 7) / 8 * 8;
     constexpr int kUB = BPC * 4;
     const int lane = threadIdx.x & 31;
+    // e[m] = this frame's record of mic m for the current chunk.  Record m of chunk c+1 is loaded into e[m] right
+    // after the last unit of chunk c that uses mic m, so the reloads are spread over the chunk and mostly complete
+    // before the next chunk needs them (a chunk-start reload stalled the producer for a full memory round trip).
+    uint32_t e[Mi][BPC];
+    auto load_rec = [&](int m, const uint8_t* base) {
+        if constexpr (BPC == 4) {
+            const uint4 v = valid ? __ldg(reinterpret_cast<const uint4*>(base + (int64_t)m * p.F_pad * kUB))
+                                  : make_uint4(0, 0, 0, 0);
+            e[m][0] = v.x;
+            e[m][1] = v.y;
+            e[m][2] = v.z;
+            e[m][3] = v.w;
+        } else {
+            const uint2 v = valid ? __ldg(reinterpret_cast<const uint2*>(base + (int64_t)m * p.F_pad * kUB))
+                                  : make_uint2(0, 0);
+            e[m][0] = v.x;
+            e[m][1] = v.y;
+        }
+    };
+    if (w.c0 < w.c1) {
+        const uint8_t* src0 = p.P16 + ((int64_t)w.c0 * Mi * p.F_pad + f) * kUB;
+#pragma unroll
+        for (int m = 0; m < Mi; ++m) load_rec(m, src0);
+    }
 #pragma unroll 1
     for (int c = w.c0; c < w.c1; ++c) {
-        uint32_t e[Mi][BPC];
         const uint8_t* src = p.P16 + ((int64_t)c * Mi * p.F_pad + f) * kUB;
+        const uint8_t* nxt = src + (int64_t)Mi * p.F_pad * kUB;
+        const bool more = c + 1 < w.c1;
+        if constexpr (BPC != 4) {          // M' = 32 (248 units): reload at the chunk start (a 32 x 248 unrolled
+            if (c != w.c0) {               // schedule of progressive loads sends e[][] to local memory)
 #pragma unroll
-        for (int m = 0; m < Mi; ++m) {
-            if constexpr (BPC == 4) {
-                uint4 v = valid ? __ldg(reinterpret_cast<const uint4*>(src + (int64_t)m * p.F_pad * kUB))
-                                : make_uint4(0, 0, 0, 0);
-                e[m][0] = v.x;
-                e[m][1] = v.y;
-                e[m][2] = v.z;
-                e[m][3] = v.w;
-            } else {
-                uint2 v = valid ? __ldg(reinterpret_cast<const uint2*>(src + (int64_t)m * p.F_pad * kUB))
-                                : make_uint2(0, 0);
-                e[m][0] = v.x;
-                e[m][1] = v.y;
+                for (int m = 0; m < Mi; ++m) load_rec(m, src);
             }
         }
         // L2 prefetch of the next chunk's records: the chunk-boundary reload then hits L2 (with N = 160 V rows the
@@ -473,6 +491,12 @@ __device__ __forceinline__ void produce_x_pair(const GemmParams& p, const Unit& 
                         outw[2 * h + 0] = outw[2 * h + 1] = 0u;
                     }
                 }
+            }
+            // records whose last use in this chunk was this unit: load the next chunk's (compile-time tests)
+            if constexpr (BPC == 4) {
+#pragma unroll
+                for (int m = 0; m < Mi; ++m)
+                    if (PT.last[m] == u && more) load_rec(m, nxt);
             }
             if constexpr (FOLD) {
                 // Re words: BPC 4 {Re k0k1, Re k2k3} = outw[0..1]; BPC 2 {Re p0, Re p1} = outw[0], outw[2].
