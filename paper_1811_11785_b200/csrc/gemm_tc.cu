@@ -1290,9 +1290,13 @@ ProjShape proj_shape(const Plan& p, int F) {
     const double slabs = (double)nc * (p.svd_fold ? p.spc_F : p.L.U / 8);
     double best_t = 1e300;
     sh.ksplit = 1;
+    static const double fixed = [] {          // per-unit fixed cost in slabs (pipeline fill + epilogue)
+        const char* e = getenv("SVDPHAT_PROJ_FIXED");
+        return e ? atof(e) : 24.0;
+    }();
     for (int S = 1; S <= p.zsplit_max && S <= nc; ++S) {
         const double waves = (double)((units * S + slots - 1) / slots);
-        const double t = waves * (slabs / S + 24.0);
+        const double t = waves * (slabs / S + fixed);
         if (t < best_t - 1e-9) {
             best_t = t;
             sh.ksplit = S;
