@@ -838,3 +838,27 @@ def test_power_maps_elementwise(cfg):
     err = np.max(np.abs(Sg - Sref), axis=1) / np.max(np.abs(Sref), axis=1).clip(1e-30)
     assert np.all(err[live] <= 2e-3), err.max()
     plan.close()
+
+
+def test_one_cta_fallbacks(monkeypatch):
+    """The 1-CTA kernels (SVDPHAT_PAIR_SRP=0: SRP GEMM with 128-row tiles, unfolded; SVDPHAT_PAIR_PROJ=0: V-on-M
+    projection, complex V) stay parity-green: all cfg1 frames, both methods, against the oracle."""
+    monkeypatch.setenv("SVDPHAT_PAIR_SRP", "0")
+    monkeypatch.setenv("SVDPHAT_PAIR_PROJ", "0")
+    w = make(1)
+    plan = _plan(w)
+    inf = plan.info()
+    assert inf["srp_rows"] == inf["Q_classes"] and inf["svd_rows"] == 2 * inf["D"]
+    audio = torch.from_numpy(w.audio).to(DEV)
+    tau = srp.tdoa(w.mics, w.points, w.fs, w.c, w.field)
+    fr, x = PP.oracle_inputs(w)
+    q, s = _run(plan, w, "srp", audio, w.n_frames)
+    keep = _check_degenerate(q, s, x)
+    P_, Y_at = PP.srp_reference(tau, x[keep], w.N)
+    PP.compare(q[keep], s[keep], P_, Y_at, "1-CTA SRP")
+    fac = svd.svd_factors(tau, w.N, w.delta)
+    q, s = _run(plan, w, "svd", audio, w.n_frames)
+    keep = _check_degenerate(q, s, x)
+    P_, Y_at = PP.svd_reference(fac, tau, x[keep], w.N)
+    PP.compare(q[keep], s[keep], P_, Y_at, "1-CTA SVD")
+    plan.close()
