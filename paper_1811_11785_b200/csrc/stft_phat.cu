@@ -7,6 +7,8 @@
 // computed in float64 at plan creation.  Output e_m[k] = X_m[k]/|X_m[k]| (0 where |X| = 0, reading R4), FP16.
 #include <cuda_fp16.h>
 
+#include <type_traits>
+
 #include "internal.h"
 
 namespace svdphat {
@@ -126,7 +128,7 @@ __device__ __forceinline__ int bitrev_r(int i) {
 // registers, twiddle, transpose through padded smem; pass 2: the 32-point DFTs over the lane index split as
 // R-point in registers x G = 32/R across lanes).  Then the real-FFT post pass, PHAT, FP16 records.
 template <int R, int BPC>
-__global__ void __launch_bounds__(32 * STFT_WARPS)
+__global__ void __launch_bounds__(32 * STFT_WARPS, R >= 32 ? 1 : 5)
     stft_phat_kernel(const float* __restrict__ audio, int64_t cs, int64_t fstride, int F, int Mi, int64_t F_pad,
                      const float* __restrict__ win, const float2* __restrict__ twN, uint8_t* __restrict__ P16,
                      int n_chunks, int k_lo, int k_hi, const uint8_t* __restrict__ mask, int64_t mask_stride) {
@@ -139,8 +141,6 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
     constexpr int WBUF = (R * SROW > H + H / 16 + 2) ? R * SROW : H + H / 16 + 2;   // float2 per warp (even)
     extern __shared__ __align__(16) uint8_t sm[];
     float2* wbuf = reinterpret_cast<float2*>(sm) + (threadIdx.x >> 5) * WBUF;
-    const int tile_stride = STFT_WARPS * 16 + 16;                                    // padded chunk row (bytes)
-    uint8_t* tile = sm + STFT_WARPS * WBUF * sizeof(float2);                        // [n_chunks][tile_stride]
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int m = blockIdx.y;
@@ -220,7 +220,13 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
     {
         constexpr int NREC = H / BPC;                                   // records of bins 0..H-1
         const bool filter = (k_lo > 0) || (k_hi < Kb) || (mask != nullptr);
-        for (int c = lane; c < NREC; c += 32) {
+        constexpr int NIT = (NREC + 31) / 32;
+        using Rec = typename std::conditional<BPC == 4, uint4, uint2>::type;
+        Rec recs[NIT];
+#pragma unroll
+        for (int it = 0; it < NIT; ++it) {
+            const int c = lane + 32 * it;
+            if (c >= NREC) break;
             float re[BPC], im[BPC];
             if (live) {
                 const int k0 = c * BPC;
@@ -263,28 +269,31 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
 #pragma unroll
                 for (int s2 = 0; s2 < BPC; ++s2) re[s2] = im[s2] = 0.f;
             }
-            uint8_t* rec = tile + c * tile_stride + warp * (BPC * 4);
             if constexpr (BPC == 4) {
                 const __half2 h0 = __floats2half2_rn(re[0], re[1]), h1 = __floats2half2_rn(re[2], re[3]);
                 const __half2 h2 = __floats2half2_rn(im[0], im[1]), h3 = __floats2half2_rn(im[2], im[3]);
-                *reinterpret_cast<uint4*>(rec) = make_uint4(*reinterpret_cast<const uint32_t*>(&h0),
-                                                            *reinterpret_cast<const uint32_t*>(&h1),
-                                                            *reinterpret_cast<const uint32_t*>(&h2),
-                                                            *reinterpret_cast<const uint32_t*>(&h3));
+                recs[it] = make_uint4(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1),
+                                      *reinterpret_cast<const uint32_t*>(&h2), *reinterpret_cast<const uint32_t*>(&h3));
             } else {
                 const __half2 h0 = __floats2half2_rn(re[0], re[1]), h1 = __floats2half2_rn(im[0], im[1]);
-                *reinterpret_cast<uint2*>(rec) = make_uint2(*reinterpret_cast<const uint32_t*>(&h0),
-                                                            *reinterpret_cast<const uint32_t*>(&h1));
+                recs[it] = make_uint2(*reinterpret_cast<const uint32_t*>(&h0), *reinterpret_cast<const uint32_t*>(&h1));
             }
         }
+        // Nyquist value before the warp's Z area is reused for its records
+        const float2 z0 = wbuf[0];
+        __syncwarp();
+        // the warp's records, in chunk order, over the start of its own (now dead) FFT buffer: no separate tile
+        Rec* myrec = reinterpret_cast<Rec*>(wbuf);
+#pragma unroll
+        for (int it = 0; it < NIT; ++it)
+            if (lane + 32 * it < NREC) myrec[lane + 32 * it] = recs[it];
         if (lane == 0) {                                                // record NREC: bin H, zero padding after it
             float e = 0.f;
             if (live && H >= k_lo && H < k_hi && (!mask || mask[(int64_t)f * mask_stride + H])) {
-                const float2 Z0 = wbuf[0];
-                const float v = Z0.x - Z0.y;
+                const float v = z0.x - z0.y;
                 e = v > 0.f ? 1.f : (v < 0.f ? -1.f : 0.f);
             }
-            __half* rec = reinterpret_cast<__half*>(tile + NREC * tile_stride + warp * (BPC * 4));
+            __half* rec = reinterpret_cast<__half*>(myrec + NREC);
 #pragma unroll
             for (int s2 = 0; s2 < 2 * BPC; ++s2) rec[s2] = __float2half_rn(0.f);
             rec[0] = __float2half_rn(e);
@@ -299,7 +308,14 @@ __global__ void __launch_bounds__(32 * STFT_WARPS)
     for (int i = threadIdx.x; i < total; i += blockDim.x) {
         const int cc = i / vec_per_chunk, wi = i % vec_per_chunk;
         uint4* out = reinterpret_cast<uint4*>(P16 + (((int64_t)cc * Mi + m) * F_pad + f0) * unit_bytes);
-        out[wi] = reinterpret_cast<const uint4*>(tile + cc * tile_stride)[wi];
+        const uint8_t* base = sm + (size_t)cc * unit_bytes;              // record cc of warp w at w*WBUF float2
+        if constexpr (BPC == 4) {
+            out[wi] = *reinterpret_cast<const uint4*>(base + (size_t)wi * WBUF * sizeof(float2));
+        } else {
+            const uint2 lo = *reinterpret_cast<const uint2*>(base + (size_t)(2 * wi) * WBUF * sizeof(float2));
+            const uint2 hi = *reinterpret_cast<const uint2*>(base + (size_t)(2 * wi + 1) * WBUF * sizeof(float2));
+            out[wi] = make_uint4(lo.x, lo.y, hi.x, hi.y);
+        }
     }
 }
 
@@ -354,7 +370,7 @@ template <int R, int BPC>
 static cudaError_t launch_rb(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F, cudaStream_t s) {
     const int H = 32 * R;
     const int wbuf = (R * 34 > H + H / 16 + 2) ? R * 34 : H + H / 16 + 2;
-    const size_t smem = STFT_WARPS * wbuf * sizeof(float2) + (size_t)p.L.n_chunks * (STFT_WARPS * 16 + 16);
+    const size_t smem = STFT_WARPS * wbuf * sizeof(float2);
     dim3 grid((F + STFT_WARPS - 1) / STFT_WARPS, p.M);
     stft_phat_kernel<R, BPC><<<grid, 32 * STFT_WARPS, smem, s>>>(audio, cs, fstride, F, p.L.Mi, p.F_pad, p.d_window,
                                                                  p.d_twN, p.d_P16, p.L.n_chunks, p.k_lo, p.k_hi,
