@@ -190,7 +190,7 @@ struct FinOut {
 };
 
 template <int NM>
-__global__ void __launch_bounds__(32 * FIN_WARPS, 3)
+__global__ void __launch_bounds__(32 * FIN_WARPS, NM == 1 ? 4 : 3)
     finalize_kernel(FinOut o, const uint8_t* __restrict__ P16, int F, int64_t F_pad, int M, int Mi, int bpc,
                     int n_chunks, int Kb, int N, const int* __restrict__ rep, const float* __restrict__ delay) {
     static_assert(NM >= 1 && NM <= 4, "1..4 results per frame");
