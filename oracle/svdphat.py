@@ -19,15 +19,69 @@ def rank_rule(sigma2_desc: np.ndarray, total: float, delta: float) -> int:
     return int(idx[0]) + 1 if idx.size else int(sigma2_desc.size)
 
 
+def gram_pass(tau: np.ndarray, N: int, x: np.ndarray | None = None, chunk: int = 2048):
+    """One pass over column chunks of W (eqs. 4, 8; W is never held whole):
+
+      G = W W^H     (the Gram matrix of eq. 10: W = U S V^H  =>  W W^H = U S^2 U^H, so its eigenpairs are the
+                     squared singular values and left singular vectors of W);
+      total = Tr{W W^H} = sum |W|^2 (eq. 11's denominator, from W itself);
+      WX = W x_f for every frame f of x, if x (F, PK) is given (eq. 9 before taking Re{}).
+
+    G is accumulated by BLAS zherk and only its upper triangle is valid.  Returns (G, total, WX or None)."""
+    from scipy.linalg import blas
+    Q, P = tau.shape
+    PK = P * (N // 2 + 1)
+    G = np.zeros((Q, Q), dtype=np.complex128, order="F")
+    WX = None if x is None else np.zeros((x.shape[0], Q), dtype=np.complex128)
+    total = 0.0
+    for c0 in range(0, PK, chunk):
+        c1 = min(PK, c0 + chunk)
+        Wc = srp.steering_cols(tau, N, c0, c1)
+        G = blas.zherk(1.0, Wc, beta=1.0, c=G, trans=0, lower=0, overwrite_c=1)
+        total += float(np.sum(Wc.real ** 2 + Wc.imag ** 2))
+        if x is not None:
+            WX += x[:, c0:c1] @ Wc.T
+    return G, total, WX
+
+
+def factors_from_gram(G: np.ndarray, total: float, delta: float, rank: int | None = None,
+                      n_top: int | None = None) -> dict:
+    """Alg. 1 offline steps 2-3 from the Gram matrix G = W W^H (upper triangle used).
+
+    Eigenpairs of G by LAPACK (scipy.linalg.eigh; only the n_top largest when n_top < Q: eq. 11 needs only the
+    leading sigma^2 because its denominator Tr{W W^H} is known exactly), descending; D by the rank rule eq. 11
+    (P:140); U_D, S_D; R = U S (eq. 13) and the normalised rows R_hat.  Raises ValueError if the
+    n_top leading eigenvalues do not reach (1 - delta) Tr{W W^H} (the caller asks for more)."""
+    import scipy.linalg
+    Q = G.shape[0]
+    n = Q if n_top is None else min(Q, int(n_top))
+    lam, Uall = scipy.linalg.eigh(G, lower=False, subset_by_index=[Q - n, Q - 1], driver="evr",
+                                  check_finite=False)
+    order = np.argsort(lam)[::-1]
+    sigma2 = np.clip(lam[order], 0.0, None)
+    if rank:
+        D = int(rank)
+    else:
+        D = rank_rule(sigma2, total, delta)
+        if n < Q and np.sum(sigma2) < (1.0 - delta) * total:
+            raise ValueError(f"the {n} leading eigenvalues hold less than 1 - delta of Tr(WW^H): ask for more")
+    U = Uall[:, order[:D]]
+    S = np.sqrt(sigma2[:D])
+    R = U * S[None, :]                                            # eq. 13 (P:152): D = U S
+    Rhat = R / np.linalg.norm(R, axis=1, keepdims=True)          # P:169
+    return dict(sigma2=sigma2, D=D, U=U, S=S, R=R, Rhat=Rhat, total=total, method="gram")
+
+
 def svd_factors(tau: np.ndarray, N: int, delta: float = 1e-5, rank: int | None = None,
-                method: str = "auto", chunk: int = 4096) -> dict:
+                method: str = "auto", chunk: int = 2048, n_top: int | None = None) -> dict:
     """Alg. 1 offline steps 1-3.
 
     method "svd": numpy/LAPACK SVD of the full W (eq. 10) - for small W.
-    method "gram": eigen-decomposition of W W^H accumulated over column chunks of W (same sigma^2 and U; V from
-                   V_D = W^H U_D S_D^{-1}), for W too large to hold (cfg3-5).  Pinned against "svd" in tests.
-    Returns dict(sigma2 (all, descending), D, U (Q,D), S (D,), V (PK,D), R = U S (eq. 13), Rhat (rows / ||row||),
-                 total = Tr{W W^H} computed from W).
+    method "gram": eigen-decomposition of W W^H accumulated over column chunks of W (gram_pass +
+                   factors_from_gram: same sigma^2 and U; V from V_D = W^H U_D S_D^{-1}), for W too large to
+                   hold (cfg3-5).  Pinned against "svd" in tests.
+    Returns dict(sigma2 (descending; all of them, or the n_top leading ones), D, U (Q,D), S (D,), V (PK,D),
+                 R = U S (eq. 13), Rhat (rows / ||row||), total = Tr{W W^H} computed from W).
     """
     Q, P = tau.shape
     K = N // 2 + 1
@@ -41,32 +95,32 @@ def svd_factors(tau: np.ndarray, N: int, delta: float = 1e-5, rank: int | None =
         total = float(np.sum(np.abs(W) ** 2))
         D = rank if rank else rank_rule(sigma2, total, delta)
         U, S, V = U[:, :D], s[:D], Vh[:D].conj().T
-    else:
-        G = np.zeros((Q, Q), dtype=np.complex128)
-        total = 0.0
-        for c0 in range(0, PK, chunk):
-            Wc = srp.steering_cols(tau, N, c0, min(PK, c0 + chunk))
-            G += Wc @ Wc.conj().T
-            total += float(np.sum(np.abs(Wc) ** 2))
-        lam, Uall = np.linalg.eigh(G)
-        order = np.argsort(lam)[::-1]
-        sigma2 = np.clip(lam[order], 0.0, None)
-        D = rank if rank else rank_rule(sigma2, total, delta)
-        U = Uall[:, order[:D]]
-        S = np.sqrt(sigma2[:D])
-        V = np.empty((PK, D), dtype=np.complex128)
-        for c0 in range(0, PK, chunk):
-            c1 = min(PK, c0 + chunk)
-            Wc = srp.steering_cols(tau, N, c0, c1)
-            V[c0:c1] = (Wc.conj().T @ U) / S[None, :]
-    R = U * S[None, :]                                            # eq. 13: D = U S
-    Rhat = R / np.linalg.norm(R, axis=1, keepdims=True)
-    return dict(sigma2=sigma2, D=D, U=U, S=S, V=V, R=R, Rhat=Rhat, total=total, method=method)
+        R = U * S[None, :]                                        # eq. 13: D = U S
+        Rhat = R / np.linalg.norm(R, axis=1, keepdims=True)
+        return dict(sigma2=sigma2, D=D, U=U, S=S, V=V, R=R, Rhat=Rhat, total=total, method=method)
+    G, total, _ = gram_pass(tau, N, chunk=chunk)
+    fac = factors_from_gram(G, total, delta, rank, n_top)
+    del G
+    U, S, D = fac["U"], fac["S"], fac["D"]
+    V = np.empty((PK, D), dtype=np.complex128)
+    for c0 in range(0, PK, chunk):
+        c1 = min(PK, c0 + chunk)
+        Wc = srp.steering_cols(tau, N, c0, c1)
+        V[c0:c1] = (Wc.conj().T @ U) / S[None, :]
+    fac["V"] = V
+    return fac
 
 
 def project(V: np.ndarray, x: np.ndarray) -> np.ndarray:
     """Eq. 12: Z = V^H X.  x (F, PK) -> Z (F, D)."""
     return x @ V.conj()
+
+
+def project_wx(fac: dict, WX: np.ndarray) -> np.ndarray:
+    """Eq. 12 with the Gram-route V_D = W^H U_D S_D^{-1} substituted (eq. 10: U_D^H W = S_D V_D^H):
+    Z_f = V_D^H x_f = S_D^{-1} U_D^H (W x_f).  WX (F, Q) = W x_f per frame (gram_pass) -> Z (F, D).  Used when
+    V_D itself (PK x D) would cost a second pass over W (cfg3/cfg4 parity); pinned against project() in tests."""
+    return (WX @ fac["U"].conj()) / fac["S"][None, :]
 
 
 def search_scores(Rhat: np.ndarray, Zhat: np.ndarray) -> np.ndarray:
