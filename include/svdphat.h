@@ -55,7 +55,22 @@ typedef struct {
     int32_t methods;           /* bitmask of SVDPHAT_METHOD_SRP | SVDPHAT_METHOD_SVD                           */
     int64_t max_frames;        /* largest n_frames of a single localize call (sizes the device workspace)       */
     int32_t device;            /* CUDA device ordinal                                                          */
+    int32_t options;           /* 0 = the product configuration; bits of SVDPHAT_OPT_* select equivalent
+                                  alternative kernels (same results up to FP32 summation order; for tests and
+                                  A/B measurements).  Unknown bits -> INVALID_ARG.                             */
 } svdphat_plan_desc;
+
+/* Plan options (svdphat_plan_desc.options).  Each selects an alternative evaluation of the same equations:
+ *   NO_SRP_FOLD   SRP GEMM on one row per steering class instead of antipodal fold rows (R22);
+ *   NO_SVD_FOLD   complex V_D (2D real-split rows) instead of the real-basis V_D of a centrally symmetric grid;
+ *   ONE_CTA_SRP   1-CTA 128-row SRP GEMM tiles instead of CTA pairs (implies NO_SRP_FOLD);
+ *   ONE_CTA_PROJ  1-CTA V-on-M projection GEMM instead of the frames-on-M CTA-pair kernel (implies NO_SVD_FOLD). */
+enum {
+    SVDPHAT_OPT_NO_SRP_FOLD = 1,
+    SVDPHAT_OPT_NO_SVD_FOLD = 2,
+    SVDPHAT_OPT_ONE_CTA_SRP = 4,
+    SVDPHAT_OPT_ONE_CTA_PROJ = 8
+};
 
 typedef struct {
     int32_t M, P, N, K_bins;   /* P = M(M-1)/2 pairs, K_bins = N/2+1                             */
@@ -84,7 +99,10 @@ typedef struct {
  * step 4 is replaced by an exhaustive contraction.  *out receives an opaque plan owned by the caller
  * (free with svdphat_plan_destroy).  Returns INVALID_ARG for bad descriptors (M<2 or >32, N not a power of two,
  * hop<=0 or >N, fs<=0, c<=0, non-finite coordinates, zero FAR direction, delta outside (0,1), methods==0,
- * max_frames<0), UNSUPPORTED if the device is not sm_100, ALLOC/TOO_LARGE if memory is insufficient. */
+ * max_frames<0, unknown option bits), UNSUPPORTED if the device is not sm_100, TOO_LARGE if the operands or the
+ * float64 setup workspace (SVD: a Q_classes^2 Gram matrix, Q_classes <= 65535) would not fit the device or the
+ * launch ranges, ALLOC if an allocation fails.  Every entry point of this header restores the caller's current CUDA
+ * device before returning (calls run on the plan's device). */
 svdphat_status svdphat_plan_create(const svdphat_plan_desc* desc, svdphat_plan_t* out);
 
 /* Fills *out (host struct).  INVALID_ARG on NULL. */

@@ -10,8 +10,14 @@ Parity status of each function:
   srpphat.cross_spectrum                pinned: identical channels -> 1, scale invariance, integer-delay phase
   srpphat.steering_rows / srp_energy    pinned: ||W||_F^2 = Q P K, Y_q <= PK, self-match, literal eq. 5 sum,
                                                 independent delay-and-sum identity, plane-wave injection
-  svdphat.rank_rule / svd_factors       pinned: paper gains 320/53/36, "svd" == "gram", rank-1 toy
+  svdphat.rank_rule / svd_factors       pinned: paper gains 320/53/36, "svd" == "gram", rank-1 toy,
+                                                V orthonormal and same subspace as LAPACK's (principal angles)
+  svdphat.gram_pass / factors_from_gram pinned: Gram == W W^H, W x == full product, top-subset eigh == LAPACK SVD
+          / project_wx                          (D, sigma^2, search scores), Z from W x == V^H x
   svdphat.svd_localize                  pinned: full rank == SRP argmax, eq. 15 identity, injection
   kdtree.KDTree                         pinned: == brute force on random/twin point sets
+  srpphat.apply_tf_mask                 pinned: all-kept = identity, fully masked frame degenerate, masked Y ==
+                                                the delay-and-sum formula over the kept bins
+  srpphat.topk_peaks                    pinned: two-source injection returns both sources
 """
 from . import kdtree, srpphat, svdphat  # noqa: F401

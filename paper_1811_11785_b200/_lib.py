@@ -18,13 +18,15 @@ METHOD_SRP, METHOD_SVD, METHOD_BOTH = 1, 2, 3
 STAGES = {1: "stft_phat", 2: "srp_gemm", 3: "svd_proj", 4: "svd_norm", 5: "svd_search", 6: "finalize"}
 _METHOD = {"srp": METHOD_SRP, "svd": METHOD_SVD, "both": METHOD_BOTH}
 DUMP_PHASORS, DUMP_Z, DUMP_CLASS_REP, DUMP_KEYS, DUMP_POWER = 1, 2, 3, 4, 5
+# svdphat_plan_desc.options: equivalent alternative kernels (tests / A-B measurements), 0 = product configuration
+OPT_NO_SRP_FOLD, OPT_NO_SVD_FOLD, OPT_ONE_CTA_SRP, OPT_ONE_CTA_PROJ = 1, 2, 4, 8
 
 
 class PlanDesc(C.Structure):
     _fields_ = [("M", C.c_int32), ("mic_xyz", C.POINTER(C.c_double)), ("fs", C.c_double), ("c", C.c_double),
                 ("N", C.c_int32), ("hop", C.c_int32), ("field", C.c_int32), ("Q", C.c_int32),
                 ("points_xyz", C.POINTER(C.c_double)), ("rank_D", C.c_int32), ("delta", C.c_double),
-                ("methods", C.c_int32), ("max_frames", C.c_int64), ("device", C.c_int32)]
+                ("methods", C.c_int32), ("max_frames", C.c_int64), ("device", C.c_int32), ("options", C.c_int32)]
 
 
 class PlanInfo(C.Structure):
@@ -101,13 +103,15 @@ class Plan:
     positions in metres (field='near', eq. 1)."""
 
     def __init__(self, mics, points, fs: float, c: float, N: int, hop: int, field: str = "far", rank_D: int = 0,
-                 delta: float = 1e-5, methods=("srp", "svd"), max_frames: int = 1024, device: int = 0):
+                 delta: float = 1e-5, methods=("srp", "svd"), max_frames: int = 1024, device: int = 0,
+                 options: int = 0):
         self._mics = np.ascontiguousarray(mics, dtype=np.float64)
         self._pts = np.ascontiguousarray(points, dtype=np.float64)
         m = (METHOD_SRP if "srp" in methods else 0) | (METHOD_SVD if "svd" in methods else 0)
         d = PlanDesc(self._mics.shape[0], self._mics.ctypes.data_as(C.POINTER(C.c_double)), fs, c, N, hop,
                      FIELD_FAR if field == "far" else FIELD_NEAR, self._pts.shape[0],
-                     self._pts.ctypes.data_as(C.POINTER(C.c_double)), rank_D, delta, m, max_frames, device)
+                     self._pts.ctypes.data_as(C.POINTER(C.c_double)), rank_D, delta, m, max_frames, device,
+                     options)
         h = C.c_void_p()
         _check(lib.svdphat_plan_create(C.byref(d), C.byref(h)), "svdphat_plan_create")
         self._h = h

@@ -8,6 +8,8 @@
 #include <cmath>
 #include <cstring>
 #include <memory>
+#include <new>
+#include <stdexcept>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -22,6 +24,59 @@ void set_error(const std::string& msg) { g_err = msg; }
 static svdphat_status fail(svdphat_status s, const std::string& msg) {
     g_err = msg;
     return s;
+}
+
+// No C++ exception crosses the C ABI: a host allocation failure (std::bad_alloc) becomes ALLOC, anything else CUDA.
+template <class Fn>
+static svdphat_status guarded(Fn&& fn) {
+    try {
+        return fn();
+    } catch (const std::bad_alloc&) {
+        return fail(SVDPHAT_ALLOC, "host allocation failed");
+    } catch (const std::exception& e) {
+        return fail(SVDPHAT_CUDA, std::string("internal error: ") + e.what());
+    } catch (...) {
+        return fail(SVDPHAT_CUDA, "internal error");
+    }
+}
+
+// Every entry point runs on the plan's device and restores the caller's current device on return.
+struct DeviceGuard {
+    int prev = -1;
+    cudaError_t err = cudaSuccess;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) err = cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur = -1;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+#define SVD_DEVICE_GUARD(dev)                                                                            \
+    DeviceGuard _dg(dev);                                                                                \
+    if (_dg.err != cudaSuccess)                                                                          \
+        return fail(SVDPHAT_CUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(_dg.err));
+
+// Allocates a pair of per-plan buffers that are used together: both or neither (a partial failure frees the first
+// and clears the runtime's sticky last-error so a later launch check does not report it).
+static bool alloc_pair(void** a, size_t na, void** b, size_t nb) {
+    if (*a && *b) return true;
+    if (*a) cudaFree(*a);
+    if (*b) cudaFree(*b);
+    *a = *b = nullptr;
+    if (cudaMalloc(a, na) != cudaSuccess) {
+        *a = nullptr;
+        cudaGetLastError();
+        return false;
+    }
+    if (cudaMalloc(b, nb) != cudaSuccess) {
+        cudaFree(*a);
+        *a = *b = nullptr;
+        cudaGetLastError();
+        return false;
+    }
+    return true;
 }
 
 // ---------------------------------------------------------------- TMA descriptor encoding (driver entry point)
@@ -90,6 +145,9 @@ static svdphat_status validate(const svdphat_plan_desc* d) {
         return fail(SVDPHAT_INVALID_ARG, "delta must be in (0, 1)");
     if (d->rank_D < 0) return fail(SVDPHAT_INVALID_ARG, "rank_D must be >= 0");
     if (d->max_frames < 0 || d->max_frames > (1ll << 26)) return fail(SVDPHAT_INVALID_ARG, "max_frames out of range");
+    if (d->options & ~(SVDPHAT_OPT_NO_SRP_FOLD | SVDPHAT_OPT_NO_SVD_FOLD | SVDPHAT_OPT_ONE_CTA_SRP |
+                       SVDPHAT_OPT_ONE_CTA_PROJ))
+        return fail(SVDPHAT_INVALID_ARG, "unknown option bits");
     for (int i = 0; i < 3 * d->M; ++i)
         if (!std::isfinite(d->mic_xyz[i])) return fail(SVDPHAT_INVALID_ARG, "non-finite microphone coordinate");
     for (int64_t q = 0; q < d->Q; ++q) {
@@ -176,11 +234,14 @@ int64_t svdphat_frame_count(int64_t L, int32_t N, int32_t hop) {
 
 void svdphat_plan_destroy(svdphat_plan_t plan) {
     if (!plan) return;
-    cudaSetDevice(plan->p.device);
-    delete plan;
+    DeviceGuard g(plan->p.device);
+    try {
+        delete plan;
+    } catch (...) {
+    }
 }
 
-svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* out) {
+static svdphat_status plan_create_impl(const svdphat_plan_desc* d, svdphat_plan_t* out) {
     if (!out) return fail(SVDPHAT_INVALID_ARG, "out is NULL");
     *out = nullptr;
     svdphat_status st = validate(d);
@@ -188,9 +249,12 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     const auto t0 = std::chrono::steady_clock::now();
 
     int ndev = 0;
-    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(SVDPHAT_UNSUPPORTED, "no CUDA device");
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        return fail(SVDPHAT_UNSUPPORTED, "no CUDA device");
+    }
     if (d->device < 0 || d->device >= ndev) return fail(SVDPHAT_INVALID_ARG, "device ordinal out of range");
-    SVD_CUDA_TRY(cudaSetDevice(d->device));
+    SVD_DEVICE_GUARD(d->device);
     cudaDeviceProp prop;
     SVD_CUDA_TRY(cudaGetDeviceProperties(&prop, d->device));
     if (prop.major != 10 || prop.minor != 0)
@@ -215,13 +279,15 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     p.max_frames = d->max_frames;
     p.F_pad = std::max<int64_t>(256, (d->max_frames + 255) / 256 * 256);
     p.L = make_layout(d->M, d->N);
-    set_band(p, 0, p.Kb, nullptr, 0);
+    p.options = d->options;
     p.trace = (double)p.Q * (double)p.P * (double)p.Kb;  // Tr{W W^H}, every |W| = 1 (eq. 4)
     p.num_sms = prop.multiProcessorCount;
 
     // ---- TDOAs in samples (float64): eq. 2 (FAR) or eq. 1 (NEAR); arrival delays
     const int M = p.M, P = p.P, Q = p.Q;
     const double k = p.fs / p.c;
+    if ((double)Q * P * 8.0 > (double)(48ll << 30))                   // host float64 TDOA table
+        return fail(SVDPHAT_TOO_LARGE, "Q * P TDOA table exceeds 48 GB of host memory");
     std::vector<double> tau((size_t)Q * P), delay((size_t)Q * M);
     const double* r = d->mic_xyz;
     for (int q = 0; q < Q; ++q) {
@@ -279,16 +345,10 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
         }
     }
     p.Q_eff = (int)p.rep_q.size();
-    {
-        const char* e = getenv("SVDPHAT_PAIR_SRP");
-        p.pair_srp = e ? atoi(e) != 0 : true;
-    }
+    p.pair_srp = !(p.options & SVDPHAT_OPT_ONE_CTA_SRP);
     p.Q_pad = p.pair_srp ? (p.Q_eff + 255) / 256 * 256 : (p.Q_eff + 127) / 128 * 128;
 
-    {
-        const char* e = getenv("SVDPHAT_PAIR_PROJ");
-        p.pair_proj = e ? atoi(e) != 0 : true;
-    }
+    p.pair_proj = !(p.options & SVDPHAT_OPT_ONE_CTA_PROJ);
     // ---- antipodal class pairs (R22): class c' is the antipode of class c when its tau row is the bitwise
     // negation of c's (far field on a centrally symmetric grid: eq. 2 is odd in s_q, so every product and sum
     // negates exactly).  Then W_c' = conj W_c (eq. 4): one SRP fold row gives both scores, and W^H W is real, so
@@ -332,13 +392,9 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
         }
     }
     const bool few_rows = 4 * (int64_t)fold_m.size() <= 3 * (int64_t)p.Q_eff;   // folding removes >= 1/4 of rows
-    {
-        const char* e = getenv("SVDPHAT_FOLD");
-        p.fold = (e ? atoi(e) != 0 : true) && p.pair_srp && (p.methods & SVDPHAT_METHOD_SRP) && few_rows;
-        const char* e2 = getenv("SVDPHAT_SVD_FOLD");
-        p.svd_fold = (e2 ? atoi(e2) != 0 : true) && p.pair_proj && (p.methods & SVDPHAT_METHOD_SVD) && few_rows &&
-                     all_paired;
-    }
+    p.fold = !(p.options & SVDPHAT_OPT_NO_SRP_FOLD) && p.pair_srp && (p.methods & SVDPHAT_METHOD_SRP) && few_rows;
+    p.svd_fold = !(p.options & SVDPHAT_OPT_NO_SVD_FOLD) && p.pair_proj && (p.methods & SVDPHAT_METHOD_SVD) &&
+                 few_rows && all_paired;
     p.fold_rows = (int)fold_m.size();
     p.spc_F = 2 * ((p.L.U + 15) / 16);
     p.K_F = (int64_t)p.L.n_chunks * p.spc_F * 64;
@@ -362,6 +418,27 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
                 p.rb_partner.push_back(fold_p[r]);
                 p.rb_kind.push_back(1);
             }
+        }
+    }
+
+    // ---- size limits (TOO_LARGE before any large allocation): the SVD setup holds a Q_classes^2 float64 Gram matrix
+    // (complex, plus its real form with a real V) and launches grids with Q_classes rows in gridDim.y
+    {
+        size_t free_b = 0, total_b = 0;
+        SVD_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+        const double n = p.Q_eff;
+        if (p.methods & SVDPHAT_METHOD_SVD) {
+            if (p.Q_eff > 65535) return fail(SVDPHAT_TOO_LARGE, "SVD setup needs Q_classes <= 65535");
+            const double gram = n * n * (16.0 + (p.svd_fold ? 8.0 : 0.0)) * 1.1;
+            if (gram > (double)free_b)
+                return fail(SVDPHAT_TOO_LARGE, "the Q_classes^2 float64 Gram matrix of the SVD setup (" +
+                                                   std::to_string((int64_t)(gram / 1e6)) + " MB) exceeds free memory");
+        }
+        if (p.methods & SVDPHAT_METHOD_SRP) {
+            const double wbytes = (double)p.W_rows * (double)p.K_W * 2.0;
+            if (wbytes > 0.9 * (double)free_b)
+                return fail(SVDPHAT_TOO_LARGE, "the FP16 steering matrix (" + std::to_string((int64_t)(wbytes / 1e6)) +
+                                                   " MB) exceeds free device memory");
         }
     }
 
@@ -491,14 +568,10 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     if ((p.methods & SVDPHAT_METHOD_BOTH) == SVDPHAT_METHOD_BOTH) {
         int lo = 0, hi = 0;
         SVD_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-        // which chain gets the SMs first after the STFT (SVDPHAT_SVD_FIRST=1: the short SVD projection, then the SRP
-        // GEMM; default: the SRP GEMM, the SVD chain filling its last wave)
-        static const bool svd_first = [] {
-            const char* e = getenv("SVDPHAT_SVD_FIRST");
-            return e && atoi(e) != 0;
-        }();
-        SVD_CUDA_TRY(cudaStreamCreateWithPriority(&p.svd_stream, cudaStreamNonBlocking, svd_first ? hi : lo));
-        SVD_CUDA_TRY(cudaStreamCreateWithPriority(&p.srp_stream, cudaStreamNonBlocking, svd_first ? lo : hi));
+        // the SRP GEMM gets the SMs first after the STFT; the SVD chain fills its last wave (r01 A/B: the reverse
+        // order was 3% slower)
+        SVD_CUDA_TRY(cudaStreamCreateWithPriority(&p.svd_stream, cudaStreamNonBlocking, lo));
+        SVD_CUDA_TRY(cudaStreamCreateWithPriority(&p.srp_stream, cudaStreamNonBlocking, hi));
         SVD_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_fork, cudaEventDisableTiming));
         SVD_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_join, cudaEventDisableTiming));
         SVD_CUDA_TRY(cudaEventCreateWithFlags(&p.ev_join2, cudaEventDisableTiming));
@@ -508,6 +581,10 @@ svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* o
     p.setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     *out = h.release();
     return SVDPHAT_OK;
+}
+
+svdphat_status svdphat_plan_create(const svdphat_plan_desc* d, svdphat_plan_t* out) {
+    return guarded([&] { return plan_create_impl(d, out); });
 }
 
 svdphat_status svdphat_plan_info(svdphat_plan_t plan, svdphat_plan_info_t* out) {
@@ -546,9 +623,9 @@ svdphat_status svdphat_plan_sigma2(svdphat_plan_t plan, double* out, int32_t n) 
     return SVDPHAT_OK;
 }
 
-static svdphat_status localize_impl(Plan& p, int32_t method, const float* d_audio, int F, int64_t channel_stride,
-                                    int64_t frame_stride, int32_t* doa_srp, float* sc_srp, int32_t* doa_svd,
-                                    float* sc_svd, cudaStream_t s) {
+static svdphat_status localize_impl(Plan& p, const Band& b, int32_t method, const float* d_audio, int F,
+                                    int64_t channel_stride, int64_t frame_stride, int32_t* doa_srp, float* sc_srp,
+                                    int32_t* doa_svd, float* sc_svd, cudaStream_t s) {
     // BOTH: after the STFT the SRP GEMM (high-priority stream) and the SVD chain (low-priority stream) run
     // concurrently: the SRP CTAs take every SM first and the SVD kernels fill the SMs its last wave releases.
     // Stage events are recorded on each kernel's own stream (an SVD stage's time may include waiting for SMs).
@@ -556,7 +633,7 @@ static svdphat_status localize_impl(Plan& p, int32_t method, const float* d_audi
     cudaStream_t sr = fork ? p.srp_stream : s, sv = fork ? p.svd_stream : s;
     SVD_CUDA_TRY(cudaMemsetAsync(p.d_keys, 0, (size_t)2 * p.F_pad * 8, s));
     SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_STFT, s,
-                        [&] { return launch_stft_phat(p, d_audio, channel_stride, frame_stride, F, s); }));
+                        [&] { return launch_stft_phat(p, b, d_audio, channel_stride, frame_stride, F, s); }));
     if (fork) {
         SVD_CUDA_TRY(cudaEventRecord(p.ev_fork, s));
         SVD_CUDA_TRY(cudaStreamWaitEvent(sr, p.ev_fork, 0));
@@ -565,12 +642,12 @@ static svdphat_status localize_impl(Plan& p, int32_t method, const float* d_audi
     int32_t* const doas[2] = {doa_srp, doa_svd};
     float* const scores[2] = {sc_srp, sc_svd};
     // SRP tail rows scored through the projection: BOTH calls on the argmax GEMM path (not the small-batch split)
-    const bool both = method == SVDPHAT_METHOD_BOTH && p.tail_n > 0 && srp_split_ways(p, F) == 1;
+    const bool both = method == SVDPHAT_METHOD_BOTH && p.tail_n > 0 && srp_split_ways(p, b, F) == 1;
     if (method & SVDPHAT_METHOD_SRP)
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_GEMM, sr, [&] { return launch_gemm(p, 0, F, sr, both); }));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_GEMM, sr, [&] { return launch_gemm(p, b, 0, F, sr, both); }));
     if (method & SVDPHAT_METHOD_SVD) {
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_PROJ, sv, [&] { return launch_gemm(p, 1, F, sv); }));
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_NORM, sv, [&] { return launch_zsplit(p, F, sv, both); }));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_PROJ, sv, [&] { return launch_gemm(p, b, 1, F, sv); }));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_NORM, sv, [&] { return launch_zsplit(p, b, F, sv, both); }));
     }
     // forked: the SRP half of the finalize runs on the SRP stream while the SVD search is still busy (after zsplit
     // when the SRP tail rows' keys come from it)
@@ -583,7 +660,7 @@ static svdphat_status localize_impl(Plan& p, int32_t method, const float* d_audi
                             [&] { return launch_finalize(p, SVDPHAT_METHOD_SRP, F, doas, scores, sr); }));
     }
     if (method & SVDPHAT_METHOD_SVD) {
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_SEARCH, sv, [&] { return launch_gemm(p, 2, F, sv); }));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_SEARCH, sv, [&] { return launch_gemm(p, b, 2, F, sv); }));
         if (fork)
             SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_FINALIZE, sv,
                                 [&] { return launch_finalize(p, SVDPHAT_METHOD_SVD, F, doas, scores, sv); }));
@@ -611,21 +688,31 @@ static svdphat_status check_localize_args(Plan& p, int32_t method, int64_t n_fra
     return SVDPHAT_OK;
 }
 
-svdphat_status svdphat_localize(svdphat_plan_t plan, int32_t method, const float* d_audio, int64_t n_frames,
-                                int64_t channel_stride, int64_t frame_stride, int32_t* d_doa, float* d_score,
-                                void* stream) {
-    if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
+// svdphat_localize and svdphat_localize_masked: validation, then the hot path on the caller's stream
+static svdphat_status localize_device(svdphat_plan_t plan, const Band& b, int32_t method, const float* d_audio,
+                                      int64_t n_frames, int64_t channel_stride, int64_t frame_stride, int32_t* d_doa,
+                                      float* d_score, void* stream) {
     Plan& p = plan->p;
     svdphat_status st = check_localize_args(p, method, n_frames, channel_stride, frame_stride);
     if (st != SVDPHAT_OK) return st;
     if (n_frames == 0) return SVDPHAT_OK;
     if (!d_audio || !d_doa || !d_score) return fail(SVDPHAT_INVALID_ARG, "NULL buffer");
     if (reinterpret_cast<uintptr_t>(d_audio) & 3) return fail(SVDPHAT_INVALID_ARG, "d_audio not 4-byte aligned");
-    SVD_CUDA_TRY(cudaSetDevice(p.device));
+    SVD_DEVICE_GUARD(p.device);
     const int F = (int)n_frames;
     const bool both = method == SVDPHAT_METHOD_BOTH;
-    return localize_impl(p, method, d_audio, F, channel_stride, frame_stride, d_doa, d_score,
+    return localize_impl(p, b, method, d_audio, F, channel_stride, frame_stride, d_doa, d_score,
                          both ? d_doa + F : d_doa, both ? d_score + F : d_score, reinterpret_cast<cudaStream_t>(stream));
+}
+
+svdphat_status svdphat_localize(svdphat_plan_t plan, int32_t method, const float* d_audio, int64_t n_frames,
+                                int64_t channel_stride, int64_t frame_stride, int32_t* d_doa, float* d_score,
+                                void* stream) {
+    if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
+    return guarded([&] {
+        return localize_device(plan, full_band(plan->p), method, d_audio, n_frames, channel_stride, frame_stride,
+                               d_doa, d_score, stream);
+    });
 }
 
 svdphat_status svdphat_localize_masked(svdphat_plan_t plan, int32_t method, const float* d_audio, int64_t n_frames,
@@ -633,20 +720,19 @@ svdphat_status svdphat_localize_masked(svdphat_plan_t plan, int32_t method, cons
                                        const uint8_t* d_mask, int64_t mask_stride, int32_t* d_doa, float* d_score,
                                        void* stream) {
     if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
-    Plan& p = plan->p;
+    const Plan& p = plan->p;
     if (k_lo < 0 || k_hi > p.Kb || k_lo >= k_hi) return fail(SVDPHAT_INVALID_ARG, "need 0 <= k_lo < k_hi <= N/2+1");
     if (mask_stride < 0) return fail(SVDPHAT_INVALID_ARG, "negative mask_stride");
-    set_band(p, k_lo, k_hi, d_mask, mask_stride);
-    const svdphat_status st = svdphat_localize(plan, method, d_audio, n_frames, channel_stride, frame_stride, d_doa,
-                                               d_score, stream);
-    set_band(p, 0, p.Kb, nullptr, 0);
-    return st;
+    const Band b = make_band(p, k_lo, k_hi, d_mask, mask_stride);     // per call; the plan is not modified
+    return guarded([&] {
+        return localize_device(plan, b, method, d_audio, n_frames, channel_stride, frame_stride, d_doa, d_score,
+                               stream);
+    });
 }
 
-svdphat_status svdphat_localize_topk(svdphat_plan_t plan, int32_t method, const float* d_audio, int64_t n_frames,
-                                     int64_t channel_stride, int64_t frame_stride, int32_t k, double min_sep_deg,
-                                     int32_t* d_doa, float* d_score, void* stream) {
-    if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
+static svdphat_status localize_topk_impl(svdphat_plan_t plan, int32_t method, const float* d_audio,
+                                         int64_t n_frames, int64_t channel_stride, int64_t frame_stride, int32_t k,
+                                         double min_sep_deg, int32_t* d_doa, float* d_score, void* stream) {
     Plan& p = plan->p;
     if (method != SVDPHAT_METHOD_SRP && method != SVDPHAT_METHOD_SVD)
         return fail(SVDPHAT_INVALID_ARG, "top-k: method must be SRP or SVD");
@@ -657,22 +743,21 @@ svdphat_status svdphat_localize_topk(svdphat_plan_t plan, int32_t method, const 
     if (p.Q_eff > 49152) return fail(SVDPHAT_INVALID_ARG, "top-k needs Q_classes <= 49152");
     if (n_frames == 0) return SVDPHAT_OK;
     if (!d_audio || !d_doa || !d_score) return fail(SVDPHAT_INVALID_ARG, "NULL buffer");
-    SVD_CUDA_TRY(cudaSetDevice(p.device));
-    if (!p.d_S) {
-        if (cudaMalloc(&p.d_S, (size_t)p.F_pad * p.Q_pad * sizeof(float)) != cudaSuccess ||
-            cudaMalloc(&p.d_cls, (size_t)p.F_pad * 4 * sizeof(int)) != cudaSuccess)
-            return fail(SVDPHAT_ALLOC, "top-k workspace allocation failed");
-    }
+    SVD_DEVICE_GUARD(p.device);
+    if (!alloc_pair(reinterpret_cast<void**>(&p.d_S), (size_t)p.F_pad * p.Q_pad * sizeof(float),
+                    reinterpret_cast<void**>(&p.d_cls), (size_t)p.F_pad * 4 * sizeof(int)))
+        return fail(SVDPHAT_ALLOC, "top-k workspace allocation failed");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int F = (int)n_frames;
+    const Band b = full_band(p);
     SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_STFT, s,
-                        [&] { return launch_stft_phat(p, d_audio, channel_stride, frame_stride, F, s); }));
+                        [&] { return launch_stft_phat(p, b, d_audio, channel_stride, frame_stride, F, s); }));
     if (method == SVDPHAT_METHOD_SRP) {
-        SVD_CUDA_TRY(launch_gemm(p, 3, F, s));
+        SVD_CUDA_TRY(launch_gemm(p, b, 3, F, s));
     } else {
-        SVD_CUDA_TRY(launch_gemm(p, 1, F, s));
-        SVD_CUDA_TRY(launch_zsplit(p, F, s));
-        SVD_CUDA_TRY(launch_gemm(p, 4, F, s));
+        SVD_CUDA_TRY(launch_gemm(p, b, 1, F, s));
+        SVD_CUDA_TRY(launch_zsplit(p, b, F, s));
+        SVD_CUDA_TRY(launch_gemm(p, b, 4, F, s));
     }
     const double kPi = 3.14159265358979323846;
     SVD_CUDA_TRY(launch_topk(p, F, k, (float)std::cos(min_sep_deg * kPi / 180.0), s));
@@ -682,12 +767,22 @@ svdphat_status svdphat_localize_topk(svdphat_plan_t plan, int32_t method, const 
     return SVDPHAT_OK;
 }
 
-svdphat_status svdphat_profile_begin(svdphat_plan_t plan, int32_t capacity) {
-    if (!plan || capacity < 0) return fail(SVDPHAT_INVALID_ARG, "bad argument");
-    Plan& p = plan->p;
-    SVD_CUDA_TRY(cudaSetDevice(p.device));
+svdphat_status svdphat_localize_topk(svdphat_plan_t plan, int32_t method, const float* d_audio, int64_t n_frames,
+                                     int64_t channel_stride, int64_t frame_stride, int32_t k, double min_sep_deg,
+                                     int32_t* d_doa, float* d_score, void* stream) {
+    if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
+    return guarded([&] {
+        return localize_topk_impl(plan, method, d_audio, n_frames, channel_stride, frame_stride, k, min_sep_deg,
+                                  d_doa, d_score, stream);
+    });
+}
+
+static svdphat_status profile_begin_impl(Plan& p, int32_t capacity) {
+    SVD_DEVICE_GUARD(p.device);
     for (cudaEvent_t e : p.prof_ev) cudaEventDestroy(e);
     p.prof_ev.assign(2 * (size_t)capacity, nullptr);
+    p.prof_on = false;
+    p.prof_cap = p.prof_n = 0;
     for (auto& e : p.prof_ev) SVD_CUDA_TRY(cudaEventCreate(&e));
     p.prof_stage.assign(capacity, 0);
     p.prof_cap = capacity;
@@ -696,13 +791,22 @@ svdphat_status svdphat_profile_begin(svdphat_plan_t plan, int32_t capacity) {
     return SVDPHAT_OK;
 }
 
+svdphat_status svdphat_profile_begin(svdphat_plan_t plan, int32_t capacity) {
+    if (!plan || capacity < 0) return fail(SVDPHAT_INVALID_ARG, "bad argument");
+    return guarded([&] { return profile_begin_impl(plan->p, capacity); });
+}
+
 int32_t svdphat_profile_end(svdphat_plan_t plan, int32_t* stage_ids, float* ms, int32_t max) {
     if (!plan) return -(int32_t)fail(SVDPHAT_INVALID_ARG, "plan is NULL");
     Plan& p = plan->p;
-    cudaSetDevice(p.device);
+    DeviceGuard g(p.device);
     int n = std::min(p.prof_n, std::max(0, max));
+    int32_t ret = n;
     for (int i = 0; i < n; ++i) {
-        if (cudaEventSynchronize(p.prof_ev[2 * i + 1]) != cudaSuccess) return -(int32_t)SVDPHAT_CUDA;
+        if (cudaEventSynchronize(p.prof_ev[2 * i + 1]) != cudaSuccess) {
+            ret = -(int32_t)SVDPHAT_CUDA;
+            break;
+        }
         float t = 0.f;
         cudaEventElapsedTime(&t, p.prof_ev[2 * i], p.prof_ev[2 * i + 1]);
         if (stage_ids) stage_ids[i] = p.prof_stage[i];
@@ -713,14 +817,12 @@ int32_t svdphat_profile_end(svdphat_plan_t plan, int32_t* stage_ids, float* ms, 
     p.prof_stage.clear();
     p.prof_on = false;
     p.prof_cap = p.prof_n = 0;
-    return n;
+    return ret;
 }
 
-svdphat_status svdphat_localize_host(svdphat_plan_t plan, int32_t method, const float* h_audio, int64_t audio_elems,
-                                     int64_t n_frames, int64_t channel_stride, int64_t frame_stride, int32_t* h_doa,
-                                     float* h_score, void* stream) {
-    if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
-    Plan& p = plan->p;
+static svdphat_status localize_host_impl(Plan& p, int32_t method, const float* h_audio, int64_t audio_elems,
+                                         int64_t n_frames, int64_t channel_stride, int64_t frame_stride,
+                                         int32_t* h_doa, float* h_score, void* stream) {
     svdphat_status st = check_localize_args(p, method, n_frames, channel_stride, frame_stride);
     if (st != SVDPHAT_OK) return st;
     if (n_frames == 0) return SVDPHAT_OK;
@@ -729,8 +831,9 @@ svdphat_status svdphat_localize_host(svdphat_plan_t plan, int32_t method, const 
     const int64_t need = M1 * channel_stride + (n_frames - 1) * frame_stride + p.N;
     if (need > audio_elems) return fail(SVDPHAT_INVALID_ARG, "audio buffer smaller than the addressed frames");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-    SVD_CUDA_TRY(cudaSetDevice(p.device));
+    SVD_DEVICE_GUARD(p.device);
     const int F = (int)n_frames;
+    const Band b = full_band(p);
     // Frame-major buffers (each frame's samples inside its own frame_stride span) are pipelined in chunks of
     // whole 256-frame tiles: the H2D of chunk i+1 (copy stream) overlaps the kernels of chunk i (caller stream).
     const int64_t span1 = M1 * channel_stride + p.N;            // elements touched by one frame
@@ -743,15 +846,16 @@ svdphat_status svdphat_localize_host(svdphat_plan_t plan, int32_t method, const 
         if (p.d_stage) cudaFree(p.d_stage);
         p.d_stage = nullptr;
         p.stage_elems = 0;
-        if (cudaMalloc(&p.d_stage, 2 * slot_elems * sizeof(float)) != cudaSuccess)
+        if (cudaMalloc(&p.d_stage, 2 * slot_elems * sizeof(float)) != cudaSuccess) {
+            p.d_stage = nullptr;
+            cudaGetLastError();
             return fail(SVDPHAT_ALLOC, "staging buffer allocation failed");
+        }
         p.stage_elems = slot_elems;
     }
-    if (!p.d_doa_stage) {
-        if (cudaMalloc(&p.d_doa_stage, 2 * p.F_pad * sizeof(int32_t)) != cudaSuccess ||
-            cudaMalloc(&p.d_score_stage, 2 * p.F_pad * sizeof(float)) != cudaSuccess)
-            return fail(SVDPHAT_ALLOC, "result staging allocation failed");
-    }
+    if (!alloc_pair(reinterpret_cast<void**>(&p.d_doa_stage), 2 * p.F_pad * sizeof(int32_t),
+                    reinterpret_cast<void**>(&p.d_score_stage), 2 * p.F_pad * sizeof(float)))
+        return fail(SVDPHAT_ALLOC, "result staging allocation failed");
     if (!p.copy_stream) {
         SVD_CUDA_TRY(cudaStreamCreateWithFlags(&p.copy_stream, cudaStreamNonBlocking));
         for (int i = 0; i < 2; ++i) {
@@ -772,8 +876,9 @@ svdphat_status svdphat_localize_host(svdphat_plan_t plan, int32_t method, const 
         SVD_CUDA_TRY(cudaMemcpyAsync(dst, h_audio + off, elems * sizeof(float), cudaMemcpyHostToDevice, p.copy_stream));
         SVD_CUDA_TRY(cudaEventRecord(p.ev_copied[slot], p.copy_stream));
         SVD_CUDA_TRY(cudaStreamWaitEvent(s, p.ev_copied[slot], 0));
-        st = localize_impl(p, method, dst, n, channel_stride, frame_stride, p.d_doa_stage + f0, p.d_score_stage + f0,
-                           p.d_doa_stage + (both ? F : 0) + f0, p.d_score_stage + (both ? F : 0) + f0, s);
+        st = localize_impl(p, b, method, dst, n, channel_stride, frame_stride, p.d_doa_stage + f0,
+                           p.d_score_stage + f0, p.d_doa_stage + (both ? F : 0) + f0,
+                           p.d_score_stage + (both ? F : 0) + f0, s);
         if (st != SVDPHAT_OK) return st;
         SVD_CUDA_TRY(cudaEventRecord(p.ev_done[slot], s));
     }
@@ -785,18 +890,26 @@ svdphat_status svdphat_localize_host(svdphat_plan_t plan, int32_t method, const 
     return SVDPHAT_OK;
 }
 
-svdphat_status svdphat_submit_host(svdphat_plan_t plan, int32_t method, const float* h_audio, int64_t audio_elems,
-                                   int64_t n_frames, int64_t channel_stride, int64_t frame_stride, int32_t* h_doa,
-                                   float* h_score, void* stream, int64_t* ticket) {
-    if (!plan || !ticket) return fail(SVDPHAT_INVALID_ARG, "NULL argument");
-    Plan& p = plan->p;
+svdphat_status svdphat_localize_host(svdphat_plan_t plan, int32_t method, const float* h_audio, int64_t audio_elems,
+                                     int64_t n_frames, int64_t channel_stride, int64_t frame_stride, int32_t* h_doa,
+                                     float* h_score, void* stream) {
+    if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
+    return guarded([&] {
+        return localize_host_impl(plan->p, method, h_audio, audio_elems, n_frames, channel_stride, frame_stride,
+                                  h_doa, h_score, stream);
+    });
+}
+
+static svdphat_status submit_host_impl(Plan& p, int32_t method, const float* h_audio, int64_t audio_elems,
+                                       int64_t n_frames, int64_t channel_stride, int64_t frame_stride, int32_t* h_doa,
+                                       float* h_score, void* stream, int64_t* ticket) {
     svdphat_status st = check_localize_args(p, method, n_frames, channel_stride, frame_stride);
     if (st != SVDPHAT_OK) return st;
     if (n_frames == 0) return fail(SVDPHAT_INVALID_ARG, "n_frames must be > 0");
     if (!h_audio || !h_doa || !h_score || audio_elems <= 0) return fail(SVDPHAT_INVALID_ARG, "NULL/empty buffer");
     const int64_t need = (int64_t)(p.M - 1) * channel_stride + (n_frames - 1) * frame_stride + p.N;
     if (need > audio_elems) return fail(SVDPHAT_INVALID_ARG, "audio buffer smaller than the addressed frames");
-    SVD_CUDA_TRY(cudaSetDevice(p.device));
+    SVD_DEVICE_GUARD(p.device);
     if (!p.up_stream) {
         SVD_CUDA_TRY(cudaStreamCreateWithFlags(&p.up_stream, cudaStreamNonBlocking));
         SVD_CUDA_TRY(cudaStreamCreateWithFlags(&p.down_stream, cudaStreamNonBlocking));
@@ -812,22 +925,23 @@ svdphat_status svdphat_submit_host(svdphat_plan_t plan, int32_t method, const fl
         if (sl.d_audio) cudaFree(sl.d_audio);
         sl.d_audio = nullptr;
         sl.elems = 0;
-        if (cudaMalloc(&sl.d_audio, need * sizeof(float)) != cudaSuccess)
+        if (cudaMalloc(&sl.d_audio, need * sizeof(float)) != cudaSuccess) {
+            sl.d_audio = nullptr;
+            cudaGetLastError();
             return fail(SVDPHAT_ALLOC, "streaming staging allocation failed");
+        }
         sl.elems = need;
     }
-    if (!sl.d_doa) {
-        if (cudaMalloc(&sl.d_doa, 2 * p.F_pad * sizeof(int32_t)) != cudaSuccess ||
-            cudaMalloc(&sl.d_score, 2 * p.F_pad * sizeof(float)) != cudaSuccess)
-            return fail(SVDPHAT_ALLOC, "streaming result allocation failed");
-    }
+    if (!alloc_pair(reinterpret_cast<void**>(&sl.d_doa), 2 * p.F_pad * sizeof(int32_t),
+                    reinterpret_cast<void**>(&sl.d_score), 2 * p.F_pad * sizeof(float)))
+        return fail(SVDPHAT_ALLOC, "streaming result allocation failed");
     cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
     const int F = (int)n_frames;
     const bool both = method == SVDPHAT_METHOD_BOTH;
     SVD_CUDA_TRY(cudaMemcpyAsync(sl.d_audio, h_audio, need * sizeof(float), cudaMemcpyHostToDevice, p.up_stream));
     SVD_CUDA_TRY(cudaEventRecord(sl.h2d, p.up_stream));
     SVD_CUDA_TRY(cudaStreamWaitEvent(s, sl.h2d, 0));
-    st = localize_impl(p, method, sl.d_audio, F, channel_stride, frame_stride, sl.d_doa, sl.d_score,
+    st = localize_impl(p, full_band(p), method, sl.d_audio, F, channel_stride, frame_stride, sl.d_doa, sl.d_score,
                        sl.d_doa + (both ? F : 0), sl.d_score + (both ? F : 0), s);
     if (st != SVDPHAT_OK) return st;
     SVD_CUDA_TRY(cudaEventRecord(sl.comp, s));
@@ -841,21 +955,29 @@ svdphat_status svdphat_submit_host(svdphat_plan_t plan, int32_t method, const fl
     return SVDPHAT_OK;
 }
 
+svdphat_status svdphat_submit_host(svdphat_plan_t plan, int32_t method, const float* h_audio, int64_t audio_elems,
+                                   int64_t n_frames, int64_t channel_stride, int64_t frame_stride, int32_t* h_doa,
+                                   float* h_score, void* stream, int64_t* ticket) {
+    if (!plan || !ticket) return fail(SVDPHAT_INVALID_ARG, "NULL argument");
+    return guarded([&] {
+        return submit_host_impl(plan->p, method, h_audio, audio_elems, n_frames, channel_stride, frame_stride, h_doa,
+                                h_score, stream, ticket);
+    });
+}
+
 svdphat_status svdphat_wait(svdphat_plan_t plan, int64_t ticket) {
     if (!plan) return fail(SVDPHAT_INVALID_ARG, "plan is NULL");
     Plan& p = plan->p;
     if (ticket < 0 || ticket >= p.next_ticket) return fail(SVDPHAT_INVALID_ARG, "unknown ticket");
     const Plan::HostSlot& sl = p.slots[ticket & 1];
     if (sl.ticket != ticket) return SVDPHAT_OK;                          // slot reused: that batch completed
-    SVD_CUDA_TRY(cudaSetDevice(p.device));
+    SVD_DEVICE_GUARD(p.device);
     SVD_CUDA_TRY(cudaEventSynchronize(sl.d2h));
     return SVDPHAT_OK;
 }
 
-svdphat_status svdphat_debug_dump(svdphat_plan_t plan, int32_t what, int64_t n_frames, void* host_out, int64_t bytes) {
-    if (!plan || !host_out) return fail(SVDPHAT_INVALID_ARG, "NULL argument");
-    Plan& p = plan->p;
-    SVD_CUDA_TRY(cudaSetDevice(p.device));
+static svdphat_status debug_dump_impl(Plan& p, int32_t what, int64_t n_frames, void* host_out, int64_t bytes) {
+    SVD_DEVICE_GUARD(p.device);
     SVD_CUDA_TRY(cudaDeviceSynchronize());
     if (n_frames < 0 || n_frames > p.last_frames) return fail(SVDPHAT_INVALID_ARG, "n_frames > frames of last call");
     const int F = (int)n_frames;
@@ -908,6 +1030,11 @@ svdphat_status svdphat_debug_dump(svdphat_plan_t plan, int32_t what, int64_t n_f
         return SVDPHAT_OK;
     }
     return fail(SVDPHAT_INVALID_ARG, "unknown dump id");
+}
+
+svdphat_status svdphat_debug_dump(svdphat_plan_t plan, int32_t what, int64_t n_frames, void* host_out, int64_t bytes) {
+    if (!plan || !host_out) return fail(SVDPHAT_INVALID_ARG, "NULL argument");
+    return guarded([&] { return debug_dump_impl(plan->p, what, n_frames, host_out, bytes); });
 }
 
 }  // extern "C"

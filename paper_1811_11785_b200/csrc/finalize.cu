@@ -334,9 +334,9 @@ cudaError_t launch_split_argmax(const Plan& p, int F, int S, cudaStream_t s) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s, bool both) {
+cudaError_t launch_zsplit(const Plan& p, const Band& b, int F, cudaStream_t s, bool both) {
     if (F <= 0) return cudaSuccess;
-    const int ldz = 2 * p.Dh, S = proj_shape(p, F).ksplit;
+    const int ldz = 2 * p.Dh, S = proj_shape(p, b, F).ksplit;
     if (ldz % 4 == 0 && ldz <= 4 * ZS_THREADS * 8) {
         const int nv = (ldz / 4 + ZS_THREADS - 1) / ZS_THREADS;
         // the tail columns always leave Z; their keys are only wanted by a BOTH call (the SRP GEMM then skips them)
@@ -469,6 +469,8 @@ __global__ void __launch_bounds__(256)
                 }
             const bool ok = i != 0x7FFFFFFF && v > -INFINITY;
             cls_out[(int64_t)f * 4 + j] = ok ? i : -1;
+            if (ok) sc[i] = -INFINITY;            // a taken class is never returned again, whatever the cone test
+                                                  // (min_sep 0: an FP32 self-dot may round below 1; a zero direction)
             sel[j] = ok ? dirs[i] : make_float4(0.f, 0.f, 0.f, 0.f);
             if (!ok) sel[j].x = 2.0f;             // no further peak: suppress nothing, later rounds also empty
         }

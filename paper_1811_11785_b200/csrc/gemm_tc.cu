@@ -47,8 +47,6 @@ struct GemmParams {
     int c_lo, c_hi;                        // active bin-chunk range (band limit, NEXT-3); producer modes only
     const int* fold_cls;                   // folded SRP (FOLD kernels): [2][fold_rows] classes of a - b / a + b
     int fold_rows;
-    int dbg;                               // timing experiments only (SVDPHAT_GEMM_DBG): 1 producer writes zeros,
-                                           // 2 TMA re-loads one W tile (results invalid)
 };
 
 // Work unit t -> output tile (m, n) and the slab / chunk range of its K split.
@@ -611,8 +609,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                     if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
 #pragma unroll
                     for (int j = 0; j < kSP; ++j) {
-                        tma_load_2d_2sm(sA + stage * kAS + j * A2_BYTES, &tmA, (p.dbg & 2) ? 0 : (ks + j) * BK,
-                                        (p.dbg & 2) ? (int)rank * 128 : w.m * 256 + (int)rank * 128, &full[stage]);
+                        tma_load_2d_2sm(sA + stage * kAS + j * A2_BYTES, &tmA, (ks + j) * BK,
+                                        w.m * 256 + (int)rank * 128, &full[stage]);
                         if (!kProducer)
                             tma_load_2d_2sm(sB + stage * kBS + j * B2_BYTES, &tmB, (ks + j) * BK,
                                             w.n * bn + (int)rank * hb, &full[stage]);
@@ -756,7 +754,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
         for (int t = pair; t < units; t += n_pairs) {
             const Unit w = unit_of(p, t);
             const int f = w.n * bn + (int)rank * hb + tp;
-            const bool valid = f < p.F && tp < hb && !(p.dbg & 1);
+            const bool valid = f < p.F && tp < hb;
             produce_x_pair<Mi, BPC, kSt, kBS, FOLD, B2_BYTES>(p, w, f, valid, sB, full, empty, stage, phase, row_off,
                                                               xr);
         }
@@ -977,240 +975,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     }
 }
 
-// ================================================================================================================
-// CTA-pair SRP GEMM with the cross-spectrum in TMEM ("TS" MMA).  Frames on M: CTA r's 4 producer warps write the
-// frames [n*256 + 128r, +128) of X straight into TMEM (lane = frame) with tcgen05.st, one 64-element K slab per
-// store, so X never touches shared memory; W is the B operand (N = 256 rows per pair, 128 per CTA) streamed by 2-SM
-// TMA.  The accumulator (128 frames x 256 rows per CTA) is reduced by a per-thread running argmax over its columns.
-// TMEM (512 cols): [0,256) accumulator, [256,512) 8-slot X ring of 32 columns.  Smem: 10-slot W ring.
-// Warps: 0 TMA (+TMEM alloc), 1 MMA (leader), 2-5 epilogue (lane groups 2,3,0,1), 6-9 producer (same groups).
-// ================================================================================================================
-constexpr int W3_STAGES = 10;
-constexpr int X3_STAGES = 8;
-constexpr int W3_BYTES = 128 * BK * 2;                 // 16 KB: this CTA's 128 rows of W per slab
-constexpr int THREADS3 = 32 * 10;
-constexpr int SMEM3_BYTES = 1024 + W3_STAGES * W3_BYTES + 512;
-
-template <int Mi, int BPC>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS3, 1)
-    gemm3_kernel(const __grid_constant__ CUtensorMap tmW, GemmParams p) {
-    constexpr int kPairs = Mi * (Mi - 1) / 2;
-    constexpr int kUnitsRaw = (BPC == 4) ? kPairs : (kPairs + 1) / 2;
-    constexpr int kU = (kUnitsRaw + 7) / 8 * 8;
-    constexpr uint32_t kIdesc = umma_idesc_f16(256, 256);
-
-    extern __shared__ __align__(1024) uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-    uint8_t* sW = smem;
-    uint64_t* wfull = reinterpret_cast<uint64_t*>(sW + W3_STAGES * W3_BYTES);
-    uint64_t* wempty = wfull + W3_STAGES;
-    uint64_t* xfull = wempty + W3_STAGES;
-    uint64_t* xempty = xfull + X3_STAGES;
-    uint64_t* tfull = xempty + X3_STAGES;
-    uint64_t* tempty = tfull + 1;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
-
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const uint32_t rank = cluster_ctarank();
-    const bool leader = rank == 0;
-    const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
-    const int units = p.m_tiles * p.n_tiles;
-
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < W3_STAGES; ++s) {
-            mbar_init(&wfull[s], 1);
-            mbar_init(&wempty[s], 1);
-        }
-        for (int s = 0; s < X3_STAGES; ++s) {
-            mbar_init(&xfull[s], 8);        // 4 producer warps x 2 CTAs (only the leader's is used)
-            mbar_init(&xempty[s], 1);
-        }
-        mbar_init(tfull, 1);
-        mbar_init(tempty, 8);               // 4 epilogue warps x 2 CTAs
-        fence_mbar_init();
-    }
-    if (warp == 0) tmem_alloc_2sm<512>(tmem_slot);
-    if (warp == 1 && lane == 0) tma_prefetch_desc(&tmW);
-    tc_fence_before();
-    __syncthreads();
-    cluster_sync();
-    tc_fence_after();
-    const uint32_t tmem_base = *tmem_slot;
-    const uint32_t tmem_x = tmem_base + 256;
-
-    if (warp == 0) {
-        if (lane == 0) {
-            int stage = 0;
-            uint32_t phase = 0;
-            for (int t = pair; t < units; t += n_pairs) {
-                const int m = t / p.n_tiles;
-                for (int ks = p.c_lo * p.spc; ks < p.c_hi * p.spc; ++ks) {
-                    mbar_wait(&wempty[stage], phase ^ 1);
-                    if (leader) mbar_arrive_expect_tx(&wfull[stage], 2 * W3_BYTES);
-                    tma_load_2d_2sm(sW + stage * W3_BYTES, &tmW, ks * BK, m * 256 + (int)rank * 128, &wfull[stage]);
-                    if (++stage == W3_STAGES) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                }
-            }
-        }
-    } else if (warp == 1) {
-        if (leader) {
-            int ws = 0, xs = 0;
-            uint32_t wph = 0, xph = 0, tph = 0;
-            for (int t = pair; t < units; t += n_pairs) {
-                mbar_wait(tempty, tph ^ 1);
-                tph ^= 1;
-                tc_fence_after();
-                for (int ks = p.c_lo * p.spc; ks < p.c_hi * p.spc; ++ks) {
-                    mbar_wait(&wfull[ws], wph);
-                    mbar_wait(&xfull[xs], xph);
-                    tc_fence_after();
-                    if (lane == 0) {
-                        const uint32_t b0 = smem_u32(sW + ws * W3_BYTES);
-                        const uint32_t a0 = tmem_x + xs * 32;
-#pragma unroll
-                        for (int kk = 0; kk < BK / 16; ++kk)
-                            umma_f16_2sm_ts(tmem_base, a0 + kk * 8, umma_desc_sw128(b0 + kk * 32), kIdesc,
-                                            (ks != p.c_lo * p.spc) || (kk != 0));
-                        umma_commit_2sm(&wempty[ws], 0x3);
-                        umma_commit_2sm(&xempty[xs], 0x3);
-                    }
-                    __syncwarp();
-                    if (++ws == W3_STAGES) {
-                        ws = 0;
-                        wph ^= 1;
-                    }
-                    if (++xs == X3_STAGES) {
-                        xs = 0;
-                        xph ^= 1;
-                    }
-                }
-                if (lane == 0) umma_commit_2sm(tfull, 0x3);
-                __syncwarp();
-            }
-        }
-    } else if (warp < 6) {
-        // ---- epilogue: lane = frame; running argmax over the 256 W rows of the tile (lowest index on ties)
-        const int g = warp & 3;
-        uint32_t tph = 0;
-        for (int t = pair; t < units; t += n_pairs) {
-            const int m = t / p.n_tiles, n = t % p.n_tiles;
-            mbar_wait(tfull, tph);
-            tph ^= 1;
-            tc_fence_after();
-            const int f = n * 256 + (int)rank * 128 + g * 32 + lane;
-            float best = -INFINITY;
-            int bi = -1;
-            const int rows_left = p.rows_valid - m * 256;
-#pragma unroll 1
-            for (int j0 = 0; j0 < 256; j0 += 32) {
-                uint32_t r[32];
-                tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + j0, r);
-                tmem_ld_wait();
-#pragma unroll
-                for (int jj = 0; jj < 32; ++jj) {
-                    const float v = __uint_as_float(r[jj]);
-                    if (j0 + jj < rows_left && v > best) {
-                        best = v;
-                        bi = j0 + jj;
-                    }
-                }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive_cluster(tempty, 0);
-            if (f < p.F && bi >= 0) atomicMax(&p.keys[f], make_key(best, (uint32_t)(m * 256 + bi)));
-        }
-    } else {
-        // ---- producer: X slabs (eqs. 3, 7) from the frame's phasors into this CTA's TMEM lanes
-        constexpr PairTab<Mi> PT{};
-        const int g = warp & 3;
-        const int row = g * 32 + lane;                                 // TMEM lane = frame row in this CTA
-        constexpr int kUB = BPC * 4;
-        int xs = 0;
-        uint32_t xph = 0;
-        for (int t = pair; t < units; t += n_pairs) {
-            const int n = t % p.n_tiles;
-            const int f = n * 256 + (int)rank * 128 + row;
-            const bool valid = f < p.F;
-#pragma unroll 1
-            for (int c = p.c_lo; c < p.c_hi; ++c) {
-                uint32_t e[Mi][BPC];
-                const uint8_t* src = p.P16 + ((int64_t)c * Mi * p.F_pad + f) * kUB;
-#pragma unroll
-                for (int mm = 0; mm < Mi; ++mm) {
-                    if constexpr (BPC == 4) {
-                        uint4 v = valid ? __ldg(reinterpret_cast<const uint4*>(src + (int64_t)mm * p.F_pad * kUB))
-                                        : make_uint4(0, 0, 0, 0);
-                        e[mm][0] = v.x;
-                        e[mm][1] = v.y;
-                        e[mm][2] = v.z;
-                        e[mm][3] = v.w;
-                    } else {
-                        uint2 v = valid ? __ldg(reinterpret_cast<const uint2*>(src + (int64_t)mm * p.F_pad * kUB))
-                                        : make_uint2(0, 0);
-                        e[mm][0] = v.x;
-                        e[mm][1] = v.y;
-                    }
-                }
-                uint32_t slab[32];
-#pragma unroll
-                for (int u = 0; u < kU; ++u) {
-                    uint32_t* o = &slab[(u & 7) * 4];
-                    if constexpr (BPC == 4) {
-                        if (u < kPairs) {
-                            const int a = PT.i[u], b = PT.j[u];
-                            const uint32_t nra01 = e[a][0] ^ 0x80008000u, nra23 = e[a][1] ^ 0x80008000u;
-                            o[0] = h2fma(e[a][0], e[b][0], h2mul(e[a][2], e[b][2]));
-                            o[1] = h2fma(e[a][1], e[b][1], h2mul(e[a][3], e[b][3]));
-                            o[2] = h2fma(e[a][2], e[b][0], h2mul(nra01, e[b][2]));
-                            o[3] = h2fma(e[a][3], e[b][1], h2mul(nra23, e[b][3]));
-                        } else {
-                            o[0] = o[1] = o[2] = o[3] = 0u;
-                        }
-                    } else {
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            const int pp = 2 * u + h;
-                            if (pp < kPairs) {
-                                const int a = PT.i[pp], b = PT.j[pp];
-                                const uint32_t nra = e[a][0] ^ 0x80008000u;
-                                o[2 * h + 0] = h2fma(e[a][0], e[b][0], h2mul(e[a][1], e[b][1]));
-                                o[2 * h + 1] = h2fma(e[a][1], e[b][0], h2mul(nra, e[b][1]));
-                            } else {
-                                o[2 * h + 0] = o[2 * h + 1] = 0u;
-                            }
-                        }
-                    }
-                    if ((u & 7) == 7) {
-                        mbar_wait(&xempty[xs], xph ^ 1);
-                        tmem_st_32x32b_x32(tmem_x + (uint32_t(g * 32) << 16) + xs * 32, slab);
-                        tmem_st_wait();
-                        tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) mbar_arrive_cluster(&xfull[xs], 0);
-                        if (++xs == X3_STAGES) {
-                            xs = 0;
-                            xph ^= 1;
-                        }
-                    }
-                }
-            }
-        }
-    }
-
-    tc_fence_before();
-    __syncthreads();
-    cluster_sync();
-    if (warp == 0) {
-        tc_fence_after();
-        tmem_dealloc_2sm<512>(tmem_base);
-    }
-}
-
 // ---------------------------------------------------------------- host side
 template <int Mi, int BPC, int MODE>
 static cudaError_t set_attr_one() {
@@ -1228,8 +992,7 @@ static cudaError_t set_attr_pair() {
     if ((e = cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, 0, true>, attr, sm))) return e;
     if ((e = cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, 1, true>, attr, sm))) return e;
     if ((e = cudaFuncSetAttribute(gemm2f_kernel<Mi, BPC, false>, attr, sm))) return e;
-    if ((e = cudaFuncSetAttribute(gemm2f_kernel<Mi, BPC, true>, attr, sm))) return e;
-    return cudaFuncSetAttribute(gemm3_kernel<Mi, BPC>, attr, SMEM3_BYTES);
+    return cudaFuncSetAttribute(gemm2f_kernel<Mi, BPC, true>, attr, sm);
 }
 
 cudaError_t gemm_set_attributes() {
@@ -1278,7 +1041,7 @@ static cudaError_t launch_one(const CUtensorMap& A, const CUtensorMap& B, const 
 }
 
 // SVD projection launch shape: CTA-pair tiles of 256 V rows (p.pair_proj) or 1-CTA tiles of 128, and its K splits
-ProjShape proj_shape(const Plan& p, int F) {
+ProjShape proj_shape(const Plan& p, const Band& b, int F) {
     ProjShape sh;
     sh.pair = p.pair_proj;
     const int f_tiles = (F + BN - 1) / BN;
@@ -1286,14 +1049,11 @@ ProjShape proj_shape(const Plan& p, int F) {
     sh.n_tiles = sh.pair ? p.proj_ntiles : f_tiles;
     const int units = sh.m_tiles * sh.n_tiles;
     const int slots = sh.pair ? p.num_sms / 2 : p.num_sms;
-    const int nc = p.c_hi - p.c_lo;
+    const int nc = b.c_hi - b.c_lo;
     const double slabs = (double)nc * (p.svd_fold ? p.spc_F : p.L.U / 8);
     double best_t = 1e300;
     sh.ksplit = 1;
-    static const double fixed = [] {          // per-unit fixed cost in slabs (pipeline fill + epilogue)
-        const char* e = getenv("SVDPHAT_PROJ_FIXED");
-        return e ? atof(e) : 24.0;
-    }();
+    constexpr double fixed = 24.0;            // per-unit fixed cost in slabs (pipeline fill + epilogue), r01 fit
     for (int S = 1; S <= p.zsplit_max && S <= nc; ++S) {
         const double waves = (double)((units * S + slots - 1) / slots);
         const double t = waves * (slabs / S + fixed);
@@ -1305,32 +1065,34 @@ ProjShape proj_shape(const Plan& p, int F) {
     return sh;
 }
 
-void set_band(Plan& p, int k_lo, int k_hi, const uint8_t* mask, int64_t mask_stride) {
-    p.k_lo = k_lo;
-    p.k_hi = k_hi;
-    p.c_lo = k_lo / p.L.bpc;
-    p.c_hi = (k_hi + p.L.bpc - 1) / p.L.bpc;
-    p.mask = mask;
-    p.mask_stride = mask_stride;
+Band make_band(const Plan& p, int k_lo, int k_hi, const uint8_t* mask, int64_t mask_stride) {
+    Band b;
+    b.k_lo = k_lo;
+    b.k_hi = k_hi;
+    b.c_lo = k_lo / p.L.bpc;
+    b.c_hi = (k_hi + p.L.bpc - 1) / p.L.bpc;
+    b.mask = mask;
+    b.mask_stride = mask_stride;
+    return b;
 }
 
 // K splits of the small-batch SRP path (fewer 256 x 256 units than half the CTA pairs), 1 = the argmax GEMM path
-int srp_split_ways(const Plan& p, int F) {
+int srp_split_ways(const Plan& p, const Band& b, int F) {
     if (!p.pair_srp || p.srp_split_max <= 1) return 1;
     const int npairs = p.num_sms / 2;
     const int units = (p.W_rows / 256) * ((F + 255) / 256);
     int S = units > 0 ? npairs / units : 1;
     S = S < p.srp_split_max ? S : p.srp_split_max;
-    S = S < p.c_hi - p.c_lo ? S : p.c_hi - p.c_lo;
+    S = S < b.c_hi - b.c_lo ? S : b.c_hi - b.c_lo;
     return (units * 2 <= npairs && S > 1) ? S : 1;
 }
 
-cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s, bool both) {
+cudaError_t launch_gemm(const Plan& p, const Band& b, int mode, int F, cudaStream_t s, bool both) {
     GemmParams gp{};
     const bool srp_mode = (mode == 0 || mode == 3);             // W16 operand (folded when p.fold)
     const bool producer_mode = srp_mode || mode == 1;
-    gp.c_lo = producer_mode ? p.c_lo : 0;
-    gp.c_hi = producer_mode ? p.c_hi : 0;
+    gp.c_lo = producer_mode ? b.c_lo : 0;
+    gp.c_hi = producer_mode ? b.c_hi : 0;
     gp.P16 = p.d_P16;
     gp.F = F;
     gp.F_pad = (int)p.F_pad;
@@ -1344,20 +1106,7 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s, bool bot
     gp.bn = BN;
     gp.fold_cls = p.d_fold_cls;
     gp.fold_rows = p.fold_rows;
-    static const int dbg = [] {
-        const char* e = getenv("SVDPHAT_GEMM_DBG");
-        return e ? atoi(e) : 0;
-    }();
-    gp.dbg = dbg;
-    static const int fixed_bn = [] {   // frames per SRP pair tile (multiple of 32, 128..256); r01: 224 (the wave-
-        const char* e = getenv("SVDPHAT_PAIR_BN");   // quantisation optimum) ran slower under the power cap than 256
-        return e ? atoi(e) : 0;
-    }();
-    static const int pf = [] {
-        const char* e = getenv("SVDPHAT_GEMM_PREFETCH");
-        return e ? atoi(e) : 1;
-    }();
-    gp.prefetch = pf;
+    gp.prefetch = 1;                   // L2 prefetch of the next chunk's phasor records (r01: +2% at cfg3)
     const CUtensorMap* A = nullptr;
     const CUtensorMap* B = &p.tm_W;  // unused placeholder for producer modes
     const int npairs = p.num_sms / 2;
@@ -1401,7 +1150,7 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s, bool bot
     int tiles = gp.m_tiles * gp.n_tiles;
     if (mode == 1) {
         // split K (at chunk boundaries) to fill the SMs, deterministic partial buffers
-        const ProjShape sh = proj_shape(p, F);
+        const ProjShape sh = proj_shape(p, b, F);
         gp.ksplit = sh.ksplit;
         if (sh.pair) {                 // frames on M, V rows on N (gemm2f_kernel)
             gp.m_tiles = sh.m_tiles;
@@ -1431,29 +1180,9 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s, bool bot
     if (tiles == 0) return cudaSuccess;
     if (mode == 2) return launch_one<4, 4, 2>(*A, *B, gp, grid, s);
     if (mode == 4) return launch_one<4, 4, 3>(*A, *B, gp, grid, s);
-    static const int ts = [] {
-        const char* e = getenv("SVDPHAT_SRP_TS");   // TS variant: correct, but 3% slower at cfg3 (r01 ncu:
-        return e ? atoi(e) : 0;                    // tensor pipe 74% active although the MMA never waits)
-    }();
-    if (mode == 0 && p.pair_srp && ts && !p.fold) {
-        gp.n_tiles = (F + 255) / 256;
-        const int units = gp.m_tiles * gp.n_tiles;
-        const int pairs = units < npairs ? units : npairs;
-#define SVD_DISPATCH3(MI, BP)                                                          \
-    if (p.L.Mi == MI) {                                                               \
-        gemm3_kernel<MI, BP><<<2 * pairs, THREADS3, SMEM3_BYTES, s>>>(*A, gp);        \
-        return cudaGetLastError();                                                    \
-    }
-        SVD_DISPATCH3(4, 4)
-        SVD_DISPATCH3(8, 4)
-        SVD_DISPATCH3(16, 4)
-        SVD_DISPATCH3(32, 2)
-#undef SVD_DISPATCH3
-        return cudaErrorInvalidValue;
-    }
-    if (mode == 0 && srp_split_ways(p, F) > 1) {
+    if (mode == 0 && srp_split_ways(p, b, F) > 1) {
         // small batch: fewer units than half the CTA pairs -> split K into chunk ranges with partial power maps
-        const int S = srp_split_ways(p, F);
+        const int S = srp_split_ways(p, b, F);
         const int units = gp.m_tiles * gp.n_tiles;
         gp.ksplit = S;
         gp.Z = p.d_Ypart;
@@ -1462,10 +1191,10 @@ cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s, bool bot
         return e != cudaSuccess ? e : launch_split_argmax(p, F, S, s);
     }
     if (mode == 0 && p.pair_srp) {
-        gp.bn = fixed_bn ? fixed_bn : 256;
+        gp.bn = 256;                   // r01: 224 (the wave-quantisation optimum) was slower under the power cap
         gp.n_tiles = (F + gp.bn - 1) / gp.bn;
         if (both && p.tail_n > 0) gp.m_tiles = p.tail_r0 / 256;   // the tail rows are scored by the projection
-        // (a BOTH call reaches here only on the argmax path: srp_split_ways(p, F) == 1, see localize_impl)
+        // (a BOTH call reaches here only on the argmax path: srp_split_ways(p, b, F) == 1, see localize_impl)
         const int units = gp.m_tiles * gp.n_tiles;
         return launch_pair<0>(p, *A, *B, gp, units < npairs ? units : npairs, p.fold, s);
     }

@@ -126,16 +126,23 @@ struct Plan {
     } slots[2];
     cudaStream_t up_stream = nullptr, down_stream = nullptr;
     int64_t next_ticket = 0;
-    // per-call band limit (NEXT-3): bins [k_lo, k_hi) -> active chunks [c_lo, c_hi); optional per-frame TF mask
-    int k_lo = 0, k_hi = 0, c_lo = 0, c_hi = 0;
-    const uint8_t* mask = nullptr;
-    int64_t mask_stride = 0;
+    int options = 0;              // svdphat_plan_desc.options (SVDPHAT_OPT_*)
     // per-stage profiling
     bool prof_on = false;
     int prof_cap = 0, prof_n = 0;
     std::vector<cudaEvent_t> prof_ev;   // 2 * prof_cap
     std::vector<int> prof_stage;
 };
+
+// Per-call band limit (NEXT-3): bins [k_lo, k_hi) -> active bin chunks [c_lo, c_hi); optional per-frame TF mask.
+// Passed explicitly to every launcher (the plan stays immutable after creation).
+struct Band {
+    int k_lo = 0, k_hi = 0, c_lo = 0, c_hi = 0;
+    const uint8_t* mask = nullptr;
+    int64_t mask_stride = 0;
+};
+Band make_band(const Plan& p, int k_lo, int k_hi, const uint8_t* mask, int64_t mask_stride);
+inline Band full_band(const Plan& p) { return make_band(p, 0, p.Kb, nullptr, 0); }
 
 // ---------------------------------------------------------------- error plumbing
 void set_error(const std::string& msg);
@@ -150,22 +157,21 @@ void set_error(const std::string& msg);
     } while (0)
 
 // ---------------------------------------------------------------- launchers (return cudaError_t)
-cudaError_t launch_stft_phat(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F,
+cudaError_t launch_stft_phat(const Plan& p, const Band& b, const float* audio, int64_t cs, int64_t fstride, int F,
                              cudaStream_t s);
 // mode: 0 = SRP argmax (A = W16, B = producer), 1 = SVD GEMM1 store Z (A = V16, B = producer),
 //       2 = SVD search argmax (A = R16, B = Zs16 via TMA), 3 = SRP power map -> d_S, 4 = SVD search power map -> d_S
 // both: a localize(BOTH) call, where the SRP tail rows travel through the projection (Plan::tail_n)
-cudaError_t launch_gemm(const Plan& p, int mode, int F, cudaStream_t s, bool both = false);
-cudaError_t launch_zsplit(const Plan& p, int F, cudaStream_t s, bool both = false);
-int srp_split_ways(const Plan& p, int F);     // > 1: the SRP call takes the small-batch split-K path
+cudaError_t launch_gemm(const Plan& p, const Band& b, int mode, int F, cudaStream_t s, bool both = false);
+cudaError_t launch_zsplit(const Plan& p, const Band& b, int F, cudaStream_t s, bool both = false);
+int srp_split_ways(const Plan& p, const Band& b, int F);   // > 1: the SRP call takes the small-batch split-K path
 cudaError_t launch_split_argmax(const Plan& p, int F, int S, cudaStream_t s);
 constexpr int MAX_KSPLIT = 32;               // cap on K splits (chunk ranges) of the store-mode GEMMs
 struct ProjShape {
     bool pair;
     int m_tiles, n_tiles, ksplit;   // pair: m = 256-frame tiles, n = proj_nt-row V tiles; 1-CTA: m = 128-row V tiles
 };
-ProjShape proj_shape(const Plan& p, int F);   // tiles and K splits of the SVD projection GEMM
-void set_band(Plan& p, int k_lo, int k_hi, const uint8_t* mask, int64_t mask_stride);
+ProjShape proj_shape(const Plan& p, const Band& b, int F);   // tiles and K splits of the SVD projection GEMM
 // method SRP|SVD|BOTH; doa[0]/score[0] receive SRP results, doa[1]/score[1] SVD results
 cudaError_t launch_finalize(const Plan& p, int method, int F, int32_t* const doa[2], float* const score[2],
                             cudaStream_t s);

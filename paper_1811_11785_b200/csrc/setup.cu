@@ -331,25 +331,15 @@ svdphat_status setup_srp_operand(Plan& p, const double* d_tau_cls) {
     return SVDPHAT_OK;
 }
 
-// V row tiling of the frames-on-M pair projection: the fewest tiles of <= 256 rows (multiples of 32) covering `rows`
-// (SVDPHAT_PROJ_NT forces the tile height, for measurements).  cfg3: real V, D = 318 -> 2 x 160; complex V, 2*D_h =
-// 640 -> 3 x 224.
+// V row tiling of the frames-on-M pair projection: the fewest tiles of <= 256 rows (multiples of 32) covering `rows`.
+// cfg3: real V, D = 318 -> 2 x 160; complex V, 2*D_h = 640 -> 3 x 224.
 static void choose_proj_tiles(Plan& p, int rows) {
     if (!p.pair_proj) {
         p.V_rows = rows;
         return;
     }
-    static const int forced = [] {
-        const char* e = getenv("SVDPHAT_PROJ_NT");
-        return e ? atoi(e) : 0;
-    }();
-    if (forced >= 32 && forced <= 256 && forced % 32 == 0) {
-        p.proj_nt = forced;
-        p.proj_ntiles = (rows + forced - 1) / forced;
-    } else {
-        p.proj_ntiles = (rows + 255) / 256;
-        p.proj_nt = ((rows + p.proj_ntiles - 1) / p.proj_ntiles + 31) / 32 * 32;
-    }
+    p.proj_ntiles = (rows + 255) / 256;
+    p.proj_nt = ((rows + p.proj_ntiles - 1) / p.proj_ntiles + 31) / 32 * 32;
     p.V_rows = p.proj_ntiles * p.proj_nt;
 }
 

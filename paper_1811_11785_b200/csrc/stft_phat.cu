@@ -367,20 +367,23 @@ __global__ void stft_phat_small_kernel(const float* __restrict__ audio, int64_t 
 }
 
 template <int R, int BPC>
-static cudaError_t launch_rb(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F, cudaStream_t s) {
+static cudaError_t launch_rb(const Plan& p, const Band& b, const float* audio, int64_t cs, int64_t fstride, int F,
+                             cudaStream_t s) {
     const int H = 32 * R;
     const int wbuf = (R * 34 > H + H / 16 + 2) ? R * 34 : H + H / 16 + 2;
     const size_t smem = STFT_WARPS * wbuf * sizeof(float2);
     dim3 grid((F + STFT_WARPS - 1) / STFT_WARPS, p.M);
     stft_phat_kernel<R, BPC><<<grid, 32 * STFT_WARPS, smem, s>>>(audio, cs, fstride, F, p.L.Mi, p.F_pad, p.d_window,
-                                                                 p.d_twN, p.d_P16, p.L.n_chunks, p.k_lo, p.k_hi,
-                                                                 p.mask, p.mask_stride);
+                                                                 p.d_twN, p.d_P16, p.L.n_chunks, b.k_lo, b.k_hi,
+                                                                 b.mask, b.mask_stride);
     return cudaGetLastError();
 }
 
 template <int R>
-static cudaError_t launch_r(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F, cudaStream_t s) {
-    return p.L.bpc == 4 ? launch_rb<R, 4>(p, audio, cs, fstride, F, s) : launch_rb<R, 2>(p, audio, cs, fstride, F, s);
+static cudaError_t launch_r(const Plan& p, const Band& b, const float* audio, int64_t cs, int64_t fstride, int F,
+                            cudaStream_t s) {
+    return p.L.bpc == 4 ? launch_rb<R, 4>(p, b, audio, cs, fstride, F, s)
+                        : launch_rb<R, 2>(p, b, audio, cs, fstride, F, s);
 }
 
 // per device: called by plan creation (cudaFuncSetAttribute applies to the current device only)
@@ -400,22 +403,22 @@ cudaError_t stft_set_attributes() {
     return e;
 }
 
-cudaError_t launch_stft_phat(const Plan& p, const float* audio, int64_t cs, int64_t fstride, int F,
+cudaError_t launch_stft_phat(const Plan& p, const Band& b, const float* audio, int64_t cs, int64_t fstride, int F,
                              cudaStream_t s) {
     if (F <= 0) return cudaSuccess;
     switch (p.N) {
-        case 64: return launch_r<1>(p, audio, cs, fstride, F, s);
-        case 128: return launch_r<2>(p, audio, cs, fstride, F, s);
-        case 256: return launch_r<4>(p, audio, cs, fstride, F, s);
-        case 512: return launch_r<8>(p, audio, cs, fstride, F, s);
-        case 1024: return launch_r<16>(p, audio, cs, fstride, F, s);
-        case 2048: return launch_r<32>(p, audio, cs, fstride, F, s);
+        case 64: return launch_r<1>(p, b, audio, cs, fstride, F, s);
+        case 128: return launch_r<2>(p, b, audio, cs, fstride, F, s);
+        case 256: return launch_r<4>(p, b, audio, cs, fstride, F, s);
+        case 512: return launch_r<8>(p, b, audio, cs, fstride, F, s);
+        case 1024: return launch_r<16>(p, b, audio, cs, fstride, F, s);
+        case 2048: return launch_r<32>(p, b, audio, cs, fstride, F, s);
         default: break;
     }
     dim3 grid((F + STFT_WARPS - 1) / STFT_WARPS, p.M);
     stft_phat_small_kernel<<<grid, 32 * STFT_WARPS, 0, s>>>(audio, cs, fstride, F, p.L.Mi, p.F_pad, p.N, p.d_window,
-                                                           p.d_twN, p.d_P16, p.L.bpc, p.L.n_chunks, p.k_lo, p.k_hi,
-                                                           p.mask, p.mask_stride);
+                                                           p.d_twN, p.d_P16, p.L.bpc, p.L.n_chunks, b.k_lo, b.k_hi,
+                                                           b.mask, b.mask_stride);
     return cudaGetLastError();
 }
 

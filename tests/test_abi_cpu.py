@@ -77,6 +77,7 @@ BAD = [
     dict(methods=()),
     dict(max_frames=-1),
     dict(rank_D=-2),
+    dict(options=16),                                  # unknown option bit
 ]
 
 
@@ -84,11 +85,11 @@ BAD = [
 def test_validation_before_device(lib, bad):
     S = lib
     kw = dict(mics=np.array([[0.05, 0, 0], [-0.05, 0, 0], [0, 0.05, 0]]), points=np.eye(3), fs=16000.0, c=343.0,
-              N=1024, hop=512, delta=1e-5, methods=("srp", "svd"), max_frames=16, rank_D=0)
+              N=1024, hop=512, delta=1e-5, methods=("srp", "svd"), max_frames=16, rank_D=0, options=0)
     kw.update(bad)
     with pytest.raises(S.SvdPhatError) as ei:
         S.Plan(kw["mics"], kw["points"], kw["fs"], kw["c"], kw["N"], kw["hop"], "far", rank_D=kw["rank_D"],
-               delta=kw["delta"], methods=kw["methods"], max_frames=kw["max_frames"])
+               delta=kw["delta"], methods=kw["methods"], max_frames=kw["max_frames"], options=kw["options"])
     assert ei.value.status == 1, str(ei.value)                  # INVALID_ARG
     assert S.lib.svdphat_last_error()
 
@@ -101,6 +102,44 @@ def test_valid_desc_without_gpu_is_unsupported(lib):
     with pytest.raises(S.SvdPhatError) as ei:
         S.Plan(np.array([[0.05, 0, 0], [-0.05, 0, 0]]), np.eye(3), 16000.0, 343.0, 64, 32)
     assert ei.value.status == 5                                   # UNSUPPORTED: no device, no CPU fallback
+
+
+def _split_worker(rank, ws, port, n_total, q):
+    """One rank of the frame-sharded run: its contiguous shard of the global frame index space, its (stand-in)
+    per-frame results, and the gather of all ranks' results to every rank (bench.frame_shard / bench.gather_frames)."""
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=ws)
+    sys.path.insert(0, ROOT)
+    import bench
+    f0, n = bench.frame_shard(n_total, rank, ws)
+    local = torch.arange(f0, f0 + n, dtype=torch.int32) * 3          # frame g's "result" = 3 g
+    allr = bench.gather_frames(local, n_total, dist)
+    q.put((rank, f0, n, allr.numpy().tolist()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("n_total", [10_001, 5])
+def test_frame_split_two_ranks(n_total):
+    """frames are sharded across ranks with no data-path collective; every frame is processed
+    by exactly one rank (contiguous, balanced shards) and the gathered results are in global frame order."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = 30500 + (os.getpid() % 1000) + n_total % 7
+    ps = [ctx.Process(target=_split_worker, args=(r, 2, port, n_total, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    for p in ps:
+        p.join(120)
+    res = sorted(q.get(timeout=10) for _ in range(2))
+    owned = np.zeros(n_total, dtype=int)
+    for _, f0, n, allr in res:
+        owned[f0:f0 + n] += 1
+        assert allr == [3 * g for g in range(n_total)]
+    assert np.all(owned == 1)
+    assert abs(res[0][2] - res[1][2]) <= 1
 
 
 def _agg_worker(rank, ws, port, q):

@@ -511,11 +511,11 @@ def test_odd_strides_same_results():
 
 
 @pytest.mark.parametrize("M", [3, 7, 12, 20])
-def test_antipodal_fold(M, monkeypatch):
+def test_antipodal_fold(M):
     """DESIGN.md R22: on a far-field grid closed under s -> -s, the SRP GEMM runs on fold rows (a class and its
     antipode share one row; Y_c = a - b, Y_c' = a + b) — half the rows — and every instantiated mic count (record
     layouts with and without a half slab pair) gives the oracle's SRP-PHAT result, the same DOAs as the unfolded
-    GEMM (SVDPHAT_FOLD=0), and the same multi-source peaks (the fold's power-map store).  A grid without central
+    GEMM (plan option NO_SRP_FOLD), and the same multi-source peaks (the fold's power-map store).  A grid without central
     symmetry is not folded."""
     from workloads import geometry as G
     from workloads import scenes as SC
@@ -529,8 +529,8 @@ def test_antipodal_fold(M, monkeypatch):
     d_audio = torch.from_numpy(audio).to(DEV)
     res = {}
     for fold in ("1", "0"):
-        monkeypatch.setenv("SVDPHAT_FOLD", fold)
-        plan = S.Plan(mics, pts, 16000.0, 343.0, N, hop, "far", methods=("srp",), max_frames=F)
+        plan = S.Plan(mics, pts, 16000.0, 343.0, N, hop, "far", methods=("srp",), max_frames=F,
+                      options=0 if fold == "1" else S.OPT_NO_SRP_FOLD)
         inf = plan.info()
         assert inf["srp_rows"] == (inf["Q_classes"] // 2 if fold == "1" else inf["Q_classes"])
         doa = torch.empty(F, dtype=torch.int32, device=DEV)
@@ -554,7 +554,6 @@ def test_antipodal_fold(M, monkeypatch):
     assert np.mean(res["1"][2] == res["0"][2]) >= 0.98
     np.testing.assert_array_equal(res["1"][1][same], res["0"][1][same])     # same q -> same eq.-5 score
     # a grid without central symmetry: no antipodes, no fold
-    monkeypatch.setenv("SVDPHAT_FOLD", "1")
     jitter = pts + rng.normal(0.0, 1e-3, pts.shape)
     plan = S.Plan(mics, jitter, 16000.0, 343.0, N, hop, "far", methods=("srp",), max_frames=F)
     inf = plan.info()
@@ -563,11 +562,11 @@ def test_antipodal_fold(M, monkeypatch):
 
 
 @pytest.mark.parametrize("M,planar", [(3, False), (7, True), (12, False), (20, False)])
-def test_real_v_projection(M, planar, monkeypatch):
+def test_real_v_projection(M, planar):
     """DESIGN.md R22 (SVD side): when every steering class has its antipode (or a zero tau row — the z axis of a
     planar array), W^H W is real, the plan takes the SVD of the real W~ = T W, and Z = V^T X runs as a fold GEMM on
     D rows.  Same D as the complex route and as the oracle, SVD-PHAT parity against the oracle's own SVD, and the same
-    DOAs as the complex-V plan (SVDPHAT_SVD_FOLD=0) up to near-ties."""
+    DOAs as the complex-V plan (plan option NO_SVD_FOLD) up to near-ties."""
     from workloads import geometry as G
     from workloads import scenes as SC
     rng = np.random.default_rng(777 + M)
@@ -582,8 +581,8 @@ def test_real_v_projection(M, planar, monkeypatch):
     d_audio = torch.from_numpy(audio).to(DEV)
     res, infos = {}, {}
     for fold in ("1", "0"):
-        monkeypatch.setenv("SVDPHAT_SVD_FOLD", fold)
-        plan = S.Plan(mics, pts, 16000.0, 343.0, N, hop, "far", methods=("svd",), max_frames=F)
+        plan = S.Plan(mics, pts, 16000.0, 343.0, N, hop, "far", methods=("svd",), max_frames=F,
+                      options=0 if fold == "1" else S.OPT_NO_SVD_FOLD)
         infos[fold] = plan.info()
         res[fold] = _run(plan, type("W", (), {"channel_stride": L, "frame_stride": hop})(), "svd", d_audio, F)
         plan.close()
@@ -752,13 +751,12 @@ def test_power_maps_elementwise(cfg):
     plan.close()
 
 
-def test_one_cta_fallbacks(monkeypatch):
-    """The 1-CTA kernels (SVDPHAT_PAIR_SRP=0: SRP GEMM with 128-row tiles, unfolded; SVDPHAT_PAIR_PROJ=0: V-on-M
+def test_one_cta_fallbacks():
+    """The 1-CTA kernels (option ONE_CTA_SRP: SRP GEMM with 128-row tiles, unfolded; ONE_CTA_PROJ: V-on-M
     projection, complex V) stay parity-green: all cfg1 frames, both methods, against the oracle."""
-    monkeypatch.setenv("SVDPHAT_PAIR_SRP", "0")
-    monkeypatch.setenv("SVDPHAT_PAIR_PROJ", "0")
     w = make(1)
-    plan = _plan(w)
+    plan = S.Plan(w.mics, w.points, w.fs, w.c, w.N, w.hop, w.field, delta=w.delta, methods=("srp", "svd"),
+                  max_frames=w.frames_per_call, options=S.OPT_ONE_CTA_SRP | S.OPT_ONE_CTA_PROJ)
     inf = plan.info()
     assert inf["srp_rows"] == inf["Q_classes"] and inf["svd_rows"] == 2 * inf["D"]
     audio = torch.from_numpy(w.audio).to(DEV)

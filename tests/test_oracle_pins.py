@@ -403,3 +403,77 @@ def test_symmetric_grid_gram_is_real():
     s_c = np.linalg.svd(W, compute_uv=False)
     s_r = np.linalg.svd(Wt, compute_uv=False)
     assert np.allclose(s_c, s_r, rtol=1e-9, atol=1e-9 * s_c[0])
+
+
+# ------------------------------------------------------------------ Gram route of eq. 10 (cfg3/cfg4 parity path)
+def test_gram_pass_top_subset_and_project_wx():
+    """The one-pass Gram route used at headline size: zherk Gram of the column chunks equals W W^H, W x per frame
+    equals the full product, the n_top-subset eigensolve gives LAPACK-SVD's D, sigma^2 and search scores (eq. 14),
+    and Z from W x (V_D^H = S^{-1} U^H W, eq. 10) equals Z = V^H x from the SVD's own V (eq. 12)."""
+    mics, grid, tau, N = _small_case(2, 64, "3d")
+    rng = np.random.default_rng(31)
+    x = srp.frames_to_x(rng.standard_normal((6, 7, N)))
+    a = svd.svd_factors(tau, N, 1e-5, method="svd")
+    G_, total, WX = svd.gram_pass(tau, N, x, chunk=97)
+    W = srp.steering_cols(tau, N, 0, tau.shape[1] * (N // 2 + 1))
+    assert np.max(np.abs(np.triu(G_) - np.triu(W @ W.conj().T))) < 1e-10 * np.abs(G_).max()
+    assert np.max(np.abs(WX - x @ W.T)) < 1e-10 * np.abs(WX).max()
+    assert total == pytest.approx(grid.shape[0] * 21 * (N // 2 + 1), rel=1e-12)
+    full = svd.factors_from_gram(G_, total, 1e-5)
+    top = svd.factors_from_gram(G_, total, 1e-5, n_top=a["D"] + 5)
+    assert a["D"] == full["D"] == top["D"]
+    n = a["D"] + 5
+    assert np.allclose(top["sigma2"][:n], a["sigma2"][:n], rtol=1e-9, atol=1e-9 * a["sigma2"][0])
+    assert np.allclose(full["sigma2"][:n], a["sigma2"][:n], rtol=1e-9, atol=1e-9 * a["sigma2"][0])
+    Za = svd.project(a["V"], x)
+    Zt = svd.project_wx(top, WX)
+    sa = svd.search_scores(a["Rhat"], Za / np.linalg.norm(Za, axis=1, keepdims=True))
+    st = svd.search_scores(top["Rhat"], Zt / np.linalg.norm(Zt, axis=1, keepdims=True))
+    assert np.max(np.abs(sa - st)) < 1e-9
+    assert np.allclose(np.linalg.norm(Za, axis=1), np.linalg.norm(Zt, axis=1), rtol=1e-10)
+    with pytest.raises(ValueError):                # too few eigenpairs to reach (1 - delta) of the trace
+        svd.factors_from_gram(G_, total, 1e-5, n_top=a["D"] - 1)
+
+
+def test_gram_route_v_is_orthonormal():
+    """Eq. 10: V_D has orthonormal columns (V^H V = I_D) and spans the same subspace as LAPACK's V (principal
+    angles 0: the singular values of V_svd^H V_gram are all 1)."""
+    mics, grid, tau, N = _small_case(2, 64, "2d")
+    a = svd.svd_factors(tau, N, 1e-5, method="svd")
+    b = svd.svd_factors(tau, N, 1e-5, method="gram", chunk=64)
+    for f in (a, b):
+        V = f["V"]
+        assert np.max(np.abs(V.conj().T @ V - np.eye(f["D"]))) < 1e-10
+    cosines = np.linalg.svd(a["V"].conj().T @ b["V"], compute_uv=False)
+    assert np.min(cosines) > 1 - 1e-10
+
+
+# ------------------------------------------------------------------ NEXT-3: binary TF masks (P:453)
+def test_tf_mask_identity_degenerate_and_delay_and_sum():
+    """apply_tf_mask: an all-kept mask is the identity; a frame with every bin masked is degenerate (R4: q = -1);
+    and the masked SRP power equals the independent delay-and-sum formula summed over the kept bins only:
+    Y_q = 1/2 sum_{k kept} (|sum_m e_m[k] exp(+j2pi k d_qm / N)|^2 - n_k)."""
+    rng = np.random.default_rng(41)
+    mics, grid, tau, N = _small_case(2, 64)
+    K, M = N // 2 + 1, 7
+    P = M * (M - 1) // 2
+    fr = rng.standard_normal((3, M, N))
+    X = srp.stft(fr)
+    x = srp.cross_spectrum(X)
+    assert np.array_equal(srp.apply_tf_mask(x, P, np.ones((3, K), bool)), x)
+    keep = rng.random((3, K)) < 0.6
+    keep[1] = False
+    xm = srp.apply_tf_mask(x, P, keep)
+    q, s = srp.srp_localize(tau, xm, N)
+    assert q[1] == -1 and s[1] == 0.0
+    Y = srp.srp_energy(tau, xm, N)
+    delay = -(FS / C) * grid @ mics.T
+    e = np.where(np.abs(X) > 0, X / np.where(np.abs(X) > 0, np.abs(X), 1), 0)
+    k = np.arange(K)
+    for f in (0, 2):
+        kk = k[keep[f]]
+        ef = e[f][:, keep[f]]
+        nk = np.sum(np.abs(ef) > 0, axis=0)
+        a = ef[None, :, :] * np.exp(2j * np.pi * kk[None, None, :] * delay[:, :, None] / N)
+        ds = 0.5 * np.sum(np.abs(a.sum(axis=1)) ** 2 - nk[None, :], axis=1)
+        assert np.max(np.abs(ds - Y[f])) < 1e-9 * np.max(np.abs(Y[f]))
