@@ -135,6 +135,28 @@ def aggregate(ms_local: float, frames_local: int, dist=None, device=None) -> tup
     return ms, fr / (ms / 1e3)
 
 
+def frame_shard(n_total: int, rank: int, ws: int) -> tuple[int, int]:
+    """Contiguous, balanced shard of the global frame index space owned by `rank`: (first frame, count).  Frames are
+    independent, so the shards need no data-path collective."""
+    base, rem = divmod(n_total, ws)
+    return rank * base + min(rank, rem), base + (1 if rank < rem else 0)
+
+
+def gather_frames(local, n_total: int, dist=None):
+    """Per-frame results of every rank's shard, concatenated in global frame order (all_gather of the shards, padded
+    to the largest shard; 8 B per frame, outside any timed region).  `local` is a 1-D tensor on the rank's device."""
+    if dist is None or not dist.is_initialized():
+        return local
+    import torch
+    ws = dist.get_world_size()
+    n_max = frame_shard(n_total, 0, ws)[1]
+    buf = torch.zeros(n_max, dtype=local.dtype, device=local.device)
+    buf[:local.numel()] = local
+    parts = [torch.empty_like(buf) for _ in range(ws)]
+    dist.all_gather(parts, buf)
+    return torch.cat([parts[r][:frame_shard(n_total, r, ws)[1]] for r in range(ws)])
+
+
 def _dist():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     if ws == 1:
