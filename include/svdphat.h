@@ -192,9 +192,10 @@ enum {
     SVDPHAT_STAGE_STFT = 1,        /* sine-window STFT + PHAT phasors                                           */
     SVDPHAT_STAGE_SRP_GEMM = 2,    /* Y = Re{W X} with fused cross-spectrum producer and argmax (eqs. 3, 5-9)   */
     SVDPHAT_STAGE_SVD_PROJ = 3,    /* Z = V^H X with fused cross-spectrum producer (eq. 12)                     */
-    SVDPHAT_STAGE_SVD_NORM = 4,    /* Zhat = Z / ||Z||, split FP16                                              */
-    SVDPHAT_STAGE_SVD_SEARCH = 5,  /* Re{Dhat_q Zhat} + fused argmax (eqs. 14-15)                               */
-    SVDPHAT_STAGE_FINALIZE = 6     /* Y_q of the chosen q (eq. 5; Alg. 1 online step 4)                         */
+    SVDPHAT_STAGE_SVD_NORM = 4,    /* Zhat = Z / ||Z|| (FP16 search operand, FP32 rescore operand)              */
+    SVDPHAT_STAGE_SVD_SEARCH = 5,  /* Re{Dhat_q Zhat} in FP16 + fused running argmax and candidate lists (eq. 14)  */
+    SVDPHAT_STAGE_FINALIZE = 6,    /* Y_q of the chosen q (eq. 5; Alg. 1 online step 4)                         */
+    SVDPHAT_STAGE_SVD_RESCORE = 7  /* exact FP32 Re{Dhat_q Zhat} of the search candidates -> q_bar (eqs. 14-15)  */
 };
 svdphat_status svdphat_profile_begin(svdphat_plan_t plan, int32_t capacity);
 int32_t svdphat_profile_end(svdphat_plan_t plan, int32_t* stage_ids, float* ms, int32_t max);

@@ -15,7 +15,8 @@ LIB_PATH = os.path.join(_HERE, "libsvdphat.so")
 OK, INVALID_ARG, ALLOC, CUDA, NUMERIC, UNSUPPORTED, TOO_LARGE = range(7)
 FIELD_FAR, FIELD_NEAR = 0, 1
 METHOD_SRP, METHOD_SVD, METHOD_BOTH = 1, 2, 3
-STAGES = {1: "stft_phat", 2: "srp_gemm", 3: "svd_proj", 4: "svd_norm", 5: "svd_search", 6: "finalize"}
+STAGES = {1: "stft_phat", 2: "srp_gemm", 3: "svd_proj", 4: "svd_norm", 5: "svd_search", 6: "finalize",
+          7: "svd_rescore"}
 _METHOD = {"srp": METHOD_SRP, "svd": METHOD_SVD, "both": METHOD_BOTH}
 DUMP_PHASORS, DUMP_Z, DUMP_CLASS_REP, DUMP_KEYS, DUMP_POWER = 1, 2, 3, 4, 5
 # svdphat_plan_desc.options: equivalent alternative kernels (tests / A-B measurements), 0 = product configuration

@@ -204,6 +204,7 @@ struct svdphat_plan_s {
         if (p.ev_z) cudaEventDestroy(p.ev_z);
         void* bufs[] = {p.d_W16,   p.d_V16,   p.d_R16,   p.d_rep,   p.d_delay,     p.d_window,      p.d_twN,
                         p.d_P16,   p.d_keys,  p.d_Z32,   p.d_Zs16,  p.d_zflag,     p.d_stage,       p.d_doa_stage,
+                        p.d_R32,   p.d_Zn32,  p.d_cand,  p.d_ccnt,
                         p.d_score_stage, p.d_S, p.d_cls, p.d_dirs, p.d_Ypart, p.d_fold_cls};
         for (void* b : bufs)
             if (b) cudaFree(b);
@@ -398,6 +399,17 @@ static svdphat_status plan_create_impl(const svdphat_plan_desc* d, svdphat_plan_
     p.fold_rows = (int)fold_m.size();
     p.spc_F = 2 * ((p.L.U + 15) / 16);
     p.K_F = (int64_t)p.L.n_chunks * p.spc_F * 64;
+    p.spc_P = (p.L.U + 15) / 16;
+    p.K_P = (int64_t)p.L.n_chunks * p.spc_P * 64;
+    // BOTH with fold + real V: the few SRP fold rows past the last full 256-row tile ride in the projection's spare V
+    // rows (a Re row and an Im row each), so the SRP GEMM skips that tile (cfg3/cfg4: 5121 = 20 x 256 + 1 rows)
+    {
+        const int nr = p.fold_rows % 256;
+        if (p.fold && p.svd_fold && p.fold_rows > 256 && nr > 0 && nr <= 8) {
+            p.tail_r0 = p.fold_rows - nr;
+            p.tail_n = nr;
+        }
+    }
     if (p.fold) {
         p.W_rows = (p.fold_rows + 255) / 256 * 256;
         p.spc_W = p.spc_F;
@@ -511,17 +523,17 @@ static svdphat_status plan_create_impl(const svdphat_plan_desc* d, svdphat_plan_
     if (p.methods & SVDPHAT_METHOD_SVD) {
         st = setup_svd_operands(p, d_tau, d->rank_D);
         if (st != SVDPHAT_OK) return st;
-        // SRP fold rows past the last full 256-row tile ride in the projection's spare V rows (BOTH calls)
-        const int nr = p.fold_rows % 256;
-        if (p.fold && p.svd_fold && p.pair_proj && p.fold_rows > 256 && nr > 0 && nr <= 8 && p.D + nr <= p.V_rows &&
-            p.D + nr <= p.Dh && 2 * p.Dh <= 4096 && p.K_W == p.K_F) {
-            p.tail_r0 = p.fold_rows - nr;
-            p.tail_n = nr;
-            SVD_CUDA_TRY(cudaMemcpy(p.d_V16 + (int64_t)p.D * p.K_F, p.d_W16 + (int64_t)p.tail_r0 * p.K_W,
-                                    (size_t)nr * p.K_F * sizeof(__half), cudaMemcpyDeviceToDevice));
-        }
-        if (!encode_2d(&p.tm_V, p.d_V16, p.V_rows, p.svd_fold ? p.K_F : p.L.K_total,
-                       p.pair_proj ? p.proj_nt / 2 : 128))
+        // the SRP tail rows' W values: Re slabs of fold row tail_r0 + r -> V row D + 2r, Im slabs -> V row D + 2r + 1
+        for (int r = 0; r < p.tail_n; ++r)
+            for (int im = 0; im < 2; ++im)
+                SVD_CUDA_TRY(cudaMemcpy2D(p.d_V16 + (int64_t)(p.D + 2 * r + im) * p.K_P, 64 * sizeof(__half),
+                                          p.d_W16 + (int64_t)(p.tail_r0 + r) * p.K_W + 64 * im, 128 * sizeof(__half),
+                                          64 * sizeof(__half), (size_t)p.L.n_chunks * p.spc_P,
+                                          cudaMemcpyDeviceToDevice));
+        p.Zh = p.svd_fold ? std::max(p.Dh, p.V_rows) : p.Dh;
+        if (2 * p.Zh > 8192) return fail(SVDPHAT_TOO_LARGE, "SVD rank too large for the Z normalisation (D <= 4000)");
+        const int v_box = !p.pair_proj ? 128 : p.svd_fold ? p.proj_nt / (2 * p.proj_nmma) : p.proj_nt / 2;
+        if (!encode_2d(&p.tm_V, p.d_V16, p.V_rows, p.svd_fold ? p.K_P : p.L.K_total, v_box))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(V) failed");
         if (!encode_2d(&p.tm_R, p.d_R16, p.Q_pad, p.K2, 128))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(R) failed");
@@ -532,11 +544,11 @@ static svdphat_status plan_create_impl(const svdphat_plan_desc* d, svdphat_plan_
     const int64_t bytes_P16 = (int64_t)p.L.n_chunks * p.L.Mi * Fp * p.L.unit_bytes;
     SVD_CUDA_TRY(cudaMalloc(&p.d_P16, bytes_P16));
     SVD_CUDA_TRY(cudaMemset(p.d_P16, 0, bytes_P16));
-    SVD_CUDA_TRY(cudaMalloc(&p.d_keys, 2 * Fp * sizeof(unsigned long long)));
-    p.bytes_ws = bytes_P16 + 2 * Fp * 8;
+    SVD_CUDA_TRY(cudaMalloc(&p.d_keys, 3 * Fp * sizeof(unsigned long long)));
+    p.bytes_ws = bytes_P16 + 3 * Fp * 8;
     if (p.methods & SVDPHAT_METHOD_SVD) {
         // split-K partial buffers: as many splits (<= MAX_KSPLIT) as fit in ~256 MB
-        const int64_t zbytes = Fp * 2 * p.Dh * (int64_t)sizeof(float);
+        const int64_t zbytes = Fp * 2 * p.Zh * (int64_t)sizeof(float);
         p.zsplit_max = (int)std::max<int64_t>(1, std::min<int64_t>(MAX_KSPLIT, (256ll << 20) / zbytes));
         SVD_CUDA_TRY(cudaMalloc(&p.d_Z32, p.zsplit_max * zbytes));
         SVD_CUDA_TRY(cudaMemset(p.d_Z32, 0, p.zsplit_max * zbytes));
@@ -544,7 +556,11 @@ static svdphat_status plan_create_impl(const svdphat_plan_desc* d, svdphat_plan_
         SVD_CUDA_TRY(cudaMemset(p.d_Zs16, 0, Fp * p.K2 * 2));
         SVD_CUDA_TRY(cudaMalloc(&p.d_zflag, Fp * sizeof(int)));
         SVD_CUDA_TRY(cudaMemset(p.d_zflag, 0, Fp * sizeof(int)));
-        p.bytes_ws += p.zsplit_max * Fp * 2 * p.Dh * 4 + Fp * p.K2 * 2 + Fp * 4;
+        SVD_CUDA_TRY(cudaMalloc(&p.d_Zn32, Fp * p.K2 * sizeof(float)));
+        SVD_CUDA_TRY(cudaMemset(p.d_Zn32, 0, Fp * p.K2 * sizeof(float)));
+        SVD_CUDA_TRY(cudaMalloc(&p.d_cand, Fp * SEARCH_CAP * sizeof(unsigned long long)));
+        SVD_CUDA_TRY(cudaMalloc(&p.d_ccnt, Fp * sizeof(int)));
+        p.bytes_ws += zbytes * p.zsplit_max + Fp * p.K2 * 6 + Fp * 8 + Fp * SEARCH_CAP * 8;
         if (!encode_2d(&p.tm_Zs, p.d_Zs16, Fp, p.K2, 256))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(Zs) failed");
     }
@@ -631,7 +647,8 @@ static svdphat_status localize_impl(Plan& p, const Band& b, int32_t method, cons
     // Stage events are recorded on each kernel's own stream (an SVD stage's time may include waiting for SMs).
     const bool fork = method == SVDPHAT_METHOD_BOTH && p.svd_stream;
     cudaStream_t sr = fork ? p.srp_stream : s, sv = fork ? p.svd_stream : s;
-    SVD_CUDA_TRY(cudaMemsetAsync(p.d_keys, 0, (size_t)2 * p.F_pad * 8, s));
+    SVD_CUDA_TRY(cudaMemsetAsync(p.d_keys, 0, (size_t)3 * p.F_pad * 8, s));
+    if (method & SVDPHAT_METHOD_SVD) SVD_CUDA_TRY(cudaMemsetAsync(p.d_ccnt, 0, (size_t)F * sizeof(int), s));
     SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_STFT, s,
                         [&] { return launch_stft_phat(p, b, d_audio, channel_stride, frame_stride, F, s); }));
     if (fork) {
@@ -661,6 +678,7 @@ static svdphat_status localize_impl(Plan& p, const Band& b, int32_t method, cons
     }
     if (method & SVDPHAT_METHOD_SVD) {
         SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_SEARCH, sv, [&] { return launch_gemm(p, b, 2, F, sv); }));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_RESCORE, sv, [&] { return launch_rescore(p, F, sv); }));
         if (fork)
             SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_FINALIZE, sv,
                                 [&] { return launch_finalize(p, SVDPHAT_METHOD_SVD, F, doas, scores, sv); }));
@@ -1002,13 +1020,13 @@ static svdphat_status debug_dump_impl(Plan& p, int32_t what, int64_t n_frames, v
     if (what == SVDPHAT_DUMP_Z) {
         if (!p.d_Z32) return fail(SVDPHAT_INVALID_ARG, "SVD not planned");
         if (bytes < (int64_t)F * 2 * p.D * 4) return fail(SVDPHAT_INVALID_ARG, "buffer too small");
-        std::vector<float> z((size_t)F * 2 * p.Dh);
+        std::vector<float> z((size_t)F * 2 * p.Zh);
         SVD_CUDA_TRY(cudaMemcpy(z.data(), p.d_Z32, z.size() * 4, cudaMemcpyDeviceToHost));
         float* o = static_cast<float*>(host_out);
         for (int f = 0; f < F; ++f)
             for (int d = 0; d < p.D; ++d) {
-                o[((size_t)f * 2 * p.D) + d] = z[(size_t)f * 2 * p.Dh + d];
-                o[((size_t)f * 2 * p.D) + p.D + d] = z[(size_t)f * 2 * p.Dh + p.Dh + d];
+                o[((size_t)f * 2 * p.D) + d] = z[(size_t)f * 2 * p.Zh + d];
+                o[((size_t)f * 2 * p.D) + p.D + d] = z[(size_t)f * 2 * p.Zh + p.Zh + d];
             }
         return SVDPHAT_OK;
     }

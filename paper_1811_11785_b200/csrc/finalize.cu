@@ -1,7 +1,7 @@
 // finalize.cu — Z normalisation/split for the search GEMM, and the per-frame finalize.
 //
-// zsplit  : Zhat = Z / ||Z|| (Alg. 1 online step 2), written as split FP16 [hi | hi | lo] so the
-//           search GEMM computes Rhat_hi.Zhat_hi + Rhat_lo.Zhat_hi + Rhat_hi.Zhat_lo (~FP32-accurate scores).
+// zsplit  : Zhat = Z / ||Z|| (Alg. 1 online step 2), written in FP16 for the search GEMM and in FP32
+//           for the exact rescore of its candidates (rescore_kernel).
 // finalize: decodes the packed argmax key (class index -> lowest point index of the class), and computes the score
 //           Y_q = Re{W_q . X} of eq. 5 for the chosen q (Alg. 1 online step 4) in the
 //           exact delay-and-sum form  Y_q = 1/2 sum_k ( |sum_m e_m[k] e^{+j 2 pi k delta_qm / N}|^2 - n_k ),
@@ -24,43 +24,15 @@ __device__ __forceinline__ uint32_t f2o_dev(float v) {   // order-preserving flo
     return (b & 0x80000000u) ? ~b : (b | 0x80000000u);
 }
 
-// Z = sum of the nsplit partial projections (fixed order: deterministic), then normalise and split.
-__global__ void zsplit_kernel(float* __restrict__ Z, int F, int64_t F_pad, int ldz, int nsplit,
-                              __half* __restrict__ Zs, int K2, int* __restrict__ zflag) {
-    const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
-    if (warp >= F) return;
-    float* z = Z + (int64_t)warp * ldz;
-    if (nsplit > 1) {
-        for (int i = lane; i < ldz; i += 32) {
-            float v = z[i];
-            for (int s = 1; s < nsplit; ++s) v += z[(int64_t)s * F_pad * ldz + i];
-            z[i] = v;
-        }
-        __syncwarp();
-    }
-    float ss = 0.f;
-    for (int i = lane; i < ldz; i += 32) ss += z[i] * z[i];
-#pragma unroll
-    for (int o = 16; o >= 1; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-    const float inv = ss > 0.f ? rsqrtf(ss) : 0.f;
-    if (lane == 0) zflag[warp] = ss > 0.f ? 0 : 1;
-    __half* out = Zs + (int64_t)warp * K2;
-    for (int i = lane; i < ldz; i += 32) {
-        const float v = z[i] * inv;
-        const __half hi = __float2half_rn(v);
-        const __half lo = __float2half_rn(v - __half2float(hi));
-        out[i] = hi;
-        out[ldz + i] = hi;
-        out[2 * ldz + i] = lo;
-    }
-}
-
-// The same, one 128-thread CTA per frame with the frame's Z held in registers (NV float4 per thread, ldz <= 512 NV):
-// every partial is read once with 16-byte loads, all NV x nsplit loads of a thread in flight together.
+// Z = sum of the nsplit partial projections (fixed order: deterministic), then Zhat = Z / ||Z||.  One 128-thread CTA
+// per frame with the frame's Z row (Z_r | Z_i, zh columns each) held in registers (NV float4 per thread, ldz <= 512 NV):
+// every partial is read once with 16-byte loads, all NV x nsplit loads of a thread in flight together.  Columns >= D of
+// each half are zero (padding V rows) except the SRP tail rows below; Zhat's first D_h columns of each half are written
+// as FP16 Zs16 [Re | Im] (search operand) and FP32 Zn32 (rescore).
 constexpr int ZS_THREADS = 128;
-// Tail (fold + real V, Plan::tail_n): columns D + r (a) and D_h + D + r (b), r < tail_n, hold the SRP fold row
-// tail_r0 + r.  They always leave Z (zeroed before the norm); for a BOTH call (keys != nullptr) they are scored
+// Tail (fold + real V, Plan::tail_n): SRP fold row tail_r0 + r rides in V rows D + 2r (its Re W values) and D + 2r + 1
+// (its Im W values), so a = Re W . x_r is column D + 2r of Z_r and b = Im W . x_i is column D + 2r + 1 of Z_i.  Columns
+// >= D always leave Z (zeroed before the norm); for a BOTH call (keys != nullptr) the tail rows are scored
 // Y_c = a - b, Y_c' = a + b into the SRP keys.
 struct ZTail {
     int n, D, r0, fold_rows;
@@ -70,13 +42,13 @@ struct ZTail {
 
 template <int NV>
 __global__ void __launch_bounds__(ZS_THREADS)
-    zsplit_cta_kernel(float* __restrict__ Z, int64_t F_pad, int ldz, int nsplit, __half* __restrict__ Zs, int K2,
-                      int* __restrict__ zflag, ZTail tail) {
+    zsplit_cta_kernel(float* __restrict__ Z, int64_t F_pad, int zh, int nsplit, __half* __restrict__ Zs,
+                      float* __restrict__ Zn, int Dh, int* __restrict__ zflag, ZTail tail) {
     __shared__ float s_ss[ZS_THREADS / 32];
     __shared__ float s_tail[2][8];
     const int f = blockIdx.x;
     const int t = threadIdx.x;
-    const int n4 = ldz >> 2;
+    const int ldz = 2 * zh, n4 = ldz >> 2;
     float4* z = reinterpret_cast<float4*>(Z + (int64_t)f * ldz);
     const int64_t split4 = F_pad * (int64_t)n4;
     float4 v[NV];
@@ -100,21 +72,19 @@ __global__ void __launch_bounds__(ZS_THREADS)
             v[j].w += w[j].w;
         }
     }
-    if (tail.n > 0) {
-        const int half = ldz >> 1;
 #pragma unroll
-        for (int j = 0; j < NV; ++j) {
-            const int i = t + ZS_THREADS * j;
-            if (i < n4) {
-                float* e = reinterpret_cast<float*>(&v[j]);
+    for (int j = 0; j < NV; ++j) {
+        const int i = t + ZS_THREADS * j;
+        if (i < n4) {
+            float* e = reinterpret_cast<float*>(&v[j]);
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    const int col = 4 * i + q;
-                    const int r = col < half ? col - tail.D : col - half - tail.D;
-                    if (r >= 0 && r < tail.n) {
-                        s_tail[col < half ? 0 : 1][r] = e[q];
-                        e[q] = 0.f;
-                    }
+            for (int q = 0; q < 4; ++q) {
+                const int col = 4 * i + q;
+                const int part = col < zh ? 0 : 1, c = col - part * zh;
+                if (c >= tail.D) {
+                    const int r = (c - tail.D - part) >> 1;         // Re rows D + 2r in Z_r, Im rows D + 2r + 1 in Z_i
+                    if (r < tail.n && c == tail.D + 2 * r + part) s_tail[part][r] = e[q];
+                    e[q] = 0.f;
                 }
             }
         }
@@ -151,24 +121,78 @@ __global__ void __launch_bounds__(ZS_THREADS)
         }
         if (best) atomicMax(&tail.keys[f], best);
     }
-    uint2* out = reinterpret_cast<uint2*>(Zs + (int64_t)f * K2);     // 4 halves per store
+    uint2* out = reinterpret_cast<uint2*>(Zs + (int64_t)f * 2 * Dh);   // 4 halves per store
+    float4* out32 = reinterpret_cast<float4*>(Zn + (int64_t)f * 2 * Dh);
 #pragma unroll
     for (int j = 0; j < NV; ++j) {
         const int i = t + ZS_THREADS * j;
-        if (i < n4) {
-            const float a[4] = {v[j].x * inv, v[j].y * inv, v[j].z * inv, v[j].w * inv};
-            __half hi[4], lo[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                hi[e] = __float2half_rn(a[e]);
-                lo[e] = __float2half_rn(a[e] - __half2float(hi[e]));
-            }
-            const uint2 h = *reinterpret_cast<const uint2*>(hi), l = *reinterpret_cast<const uint2*>(lo);
-            out[i] = h;
-            out[n4 + i] = h;
-            out[2 * n4 + i] = l;
+        const int col = 4 * i;
+        const int part = col < zh ? 0 : 1, c = col - part * zh;
+        if (i < n4 && c < Dh) {
+            const float4 a = make_float4(v[j].x * inv, v[j].y * inv, v[j].z * inv, v[j].w * inv);
+            __half h[4] = {__float2half_rn(a.x), __float2half_rn(a.y), __float2half_rn(a.z), __float2half_rn(a.w)};
+            const int o4 = (part * Dh + c) >> 2;
+            out[o4] = *reinterpret_cast<const uint2*>(h);
+            out32[o4] = a;
         }
     }
+}
+
+// Exact rescore of the FP16 search (eqs. 14-15 in FP32): warp per frame; the candidates of the search GEMM whose FP16
+// score is within SEARCH_TAU of the frame's FP16 maximum are rescored as Re{Dhat_q . Zhat} = R32[q] . Zn32[f] in FP32
+// and the best (lowest class on ties) becomes the frame's SVD key.  A frame whose list overflowed (more than
+// SEARCH_CAP entries) is rescored over every class.  The key does not depend on the candidates' order.
+__global__ void rescore_kernel(const unsigned long long* __restrict__ keys16, const unsigned long long* __restrict__ cand,
+                               const int* __restrict__ ccnt, const float* __restrict__ R32,
+                               const float* __restrict__ Zn, int K2, int Q, int F,
+                               unsigned long long* __restrict__ keys) {
+    const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (f >= F) return;
+    const unsigned long long k16 = keys16[f];
+    if (k16 == 0ull) {
+        if (lane == 0) keys[f] = 0ull;
+        return;
+    }
+    const float4* zf = reinterpret_cast<const float4*>(Zn + (int64_t)f * K2);
+    const int n4 = K2 >> 2;
+    auto score = [&](int q) {
+        const float4* r = reinterpret_cast<const float4*>(R32 + (int64_t)q * K2);
+        float acc = 0.f;
+        for (int i = lane; i < n4; i += 32) {
+            const float4 a = __ldg(r + i), b = zf[i];
+            acc = fmaf(a.x, b.x, acc);
+            acc = fmaf(a.y, b.y, acc);
+            acc = fmaf(a.z, b.z, acc);
+            acc = fmaf(a.w, b.w, acc);
+        }
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        return acc;                                   // identical in every lane (butterfly)
+    };
+    unsigned long long best = 0ull;
+    const int n = ccnt[f];
+    if (n <= SEARCH_CAP) {
+        const uint32_t o16 = (uint32_t)(k16 >> 32);
+        const float m16 = __uint_as_float((o16 & 0x80000000u) ? (o16 & 0x7FFFFFFFu) : ~o16);
+        for (int c = 0; c < n; ++c) {
+            const unsigned long long e = cand[(int64_t)f * SEARCH_CAP + c];
+            const uint32_t oe = (uint32_t)(e >> 32);
+            const float s16 = __uint_as_float((oe & 0x80000000u) ? (oe & 0x7FFFFFFFu) : ~oe);
+            if (s16 < m16 - SEARCH_TAU) continue;
+            const int q = (int)(0xFFFFFFFFu - (uint32_t)(e & 0xFFFFFFFFull));
+            const float v = score(q);
+            const unsigned long long kq = v == v ? ((unsigned long long)f2o_dev(v) << 32) | (0xFFFFFFFFull - q) : 0ull;
+            best = kq > best ? kq : best;
+        }
+    } else {
+        for (int q = 0; q < Q; ++q) {
+            const float v = score(q);
+            const unsigned long long kq = v == v ? ((unsigned long long)f2o_dev(v) << 32) | (0xFFFFFFFFull - q) : 0ull;
+            best = kq > best ? kq : best;
+        }
+    }
+    if (lane == 0) keys[f] = best;
 }
 
 // CTA = 8 consecutive frames x 8 warps; lane = (chunk sub-slot lane>>3, frame lane&7), so a warp's record loads are
@@ -336,24 +360,29 @@ cudaError_t launch_split_argmax(const Plan& p, int F, int S, cudaStream_t s) {
 
 cudaError_t launch_zsplit(const Plan& p, const Band& b, int F, cudaStream_t s, bool both) {
     if (F <= 0) return cudaSuccess;
-    const int ldz = 2 * p.Dh, S = proj_shape(p, b, F).ksplit;
-    if (ldz % 4 == 0 && ldz <= 4 * ZS_THREADS * 8) {
-        const int nv = (ldz / 4 + ZS_THREADS - 1) / ZS_THREADS;
-        // the tail columns always leave Z; their keys are only wanted by a BOTH call (the SRP GEMM then skips them)
-        const ZTail tl{p.tail_n, p.D, p.tail_r0, p.fold_rows, p.d_fold_cls, both ? p.d_keys : nullptr};
-        if (nv <= 1)
-            zsplit_cta_kernel<1><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag, tl);
-        else if (nv <= 2)
-            zsplit_cta_kernel<2><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag, tl);
-        else if (nv <= 4)
-            zsplit_cta_kernel<4><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag, tl);
-        else
-            zsplit_cta_kernel<8><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag, tl);
-        return cudaGetLastError();
+    const int ldz = 2 * p.Zh, S = proj_shape(p, b, F).ksplit;
+    const int nv = (ldz / 4 + ZS_THREADS - 1) / ZS_THREADS;
+    // the tail columns always leave Z; their keys are only wanted by a BOTH call (the SRP GEMM then skips them)
+    const ZTail tl{p.tail_n, p.D, p.tail_r0, p.fold_rows, p.d_fold_cls, both ? p.d_keys : nullptr};
+#define SVD_ZS(NV)                                                                                                  \
+    if (nv <= NV) {                                                                                                 \
+        zsplit_cta_kernel<NV><<<F, ZS_THREADS, 0, s>>>(p.d_Z32, p.F_pad, p.Zh, S, p.d_Zs16, p.d_Zn32, p.Dh,          \
+                                                       p.d_zflag, tl);                                             \
+        return cudaGetLastError();                                                                                  \
     }
-    const int threads = 256;
-    const int blocks = (F * 32 + threads - 1) / threads;
-    zsplit_kernel<<<blocks, threads, 0, s>>>(p.d_Z32, F, p.F_pad, ldz, S, p.d_Zs16, p.K2, p.d_zflag);
+    SVD_ZS(1)
+    SVD_ZS(2)
+    SVD_ZS(4)
+    SVD_ZS(8)
+    SVD_ZS(16)
+#undef SVD_ZS
+    return cudaErrorInvalidValue;                 // 2*Zh > 8192 columns: excluded at plan creation
+}
+
+cudaError_t launch_rescore(const Plan& p, int F, cudaStream_t s) {
+    if (F <= 0) return cudaSuccess;
+    rescore_kernel<<<(F * 32 + 255) / 256, 256, 0, s>>>(p.d_keys + 2 * p.F_pad, p.d_cand, p.d_ccnt, p.d_R32,
+                                                        p.d_Zn32, p.K2, p.Q_eff, F, p.d_keys + p.F_pad);
     return cudaGetLastError();
 }
 

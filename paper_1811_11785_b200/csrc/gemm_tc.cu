@@ -47,6 +47,11 @@ struct GemmParams {
     int c_lo, c_hi;                        // active bin-chunk range (band limit, NEXT-3); producer modes only
     const int* fold_cls;                   // folded SRP (FOLD kernels): [2][fold_rows] classes of a - b / a + b
     int fold_rows;
+    // part projection (gemm2p_kernel): ring stages, stage bytes, MMAs per K step and their N, Z_i column offset
+    int stages, stage_bytes, n_mma, nmma, zh;
+    // FP16 search (mode 2): candidate lists (FP16 score, class) of rows within SEARCH_TAU of the running maximum
+    unsigned long long* cand;
+    int* ccnt;
 };
 
 // Work unit t -> output tile (m, n) and the slab / chunk range of its K split.
@@ -269,7 +274,25 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
                         k[jj] = (row_ok && v == v) ? make_key(v, (uint32_t)row) : 0ull;
                     }
                     const unsigned long long best = transpose_max32(k, lane);
-                    if (f0 + lane < p.F && best != 0ull) atomicMax(&p.keys[f0 + lane], best);
+                    const bool fok = f0 + lane < p.F;
+                    unsigned long long run = 0ull;                 // running maximum of this frame (lane's column)
+                    if (fok && best != 0ull) run = atomicMax(&p.keys[f0 + lane], best);
+                    if (MODE == 2) {
+                        // candidates of the exact rescore: rows within SEARCH_TAU of the running FP16 maximum.  The
+                        // exact argmax q* has s16(q*) >= max16 - 2e >= running - SEARCH_TAU, e the FP16 error bound.
+                        run = run > best ? run : best;
+                        const float thr = run ? o2f((uint32_t)(run >> 32)) - SEARCH_TAU : INFINITY;
+#pragma unroll
+                        for (int jj = 0; jj < 32; ++jj) {
+                            const float t = __shfl_sync(0xffffffffu, thr, jj);
+                            const float v = __uint_as_float(r[jj]);
+                            if (row_ok && v >= t && f0 + jj < p.F) {
+                                const int idx = atomicAdd(&p.ccnt[f0 + jj], 1);
+                                if (idx < SEARCH_CAP)
+                                    p.cand[(int64_t)(f0 + jj) * SEARCH_CAP + idx] = make_key(v, (uint32_t)row);
+                            }
+                        }
+                    }
                 }
             }
             tc_fence_before();
@@ -770,30 +793,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
 }
 
 // ================================================================================================================
-// SVD projection on CTA pairs with frames on M (eq. 12): Z[f, r] = sum_kappa x16[f,kappa] V16[r,kappa].
-// A = this CTA's 128 frames of X from the producer warps (produce_x_pair), B = proj_nt rows of V16 per pair tile
-// (proj_nt/2 per CTA, 2-SM TMA), N = proj_nt chosen at plan creation to cover the V rows tightly (cfg3 real V:
-// 2 x 160 = 320 rows for D = 318, where 256-row M tiles needed 512).  The accumulator lane is a frame and its
-// columns are V rows, so each thread writes a contiguous segment of its frame's Z row.  FOLD (real V, R22): slabs
-// alternate Re (accumulator a -> Z_r, column d) and Im (b -> Z_i, column D_h + d).  Warps as gemm2_kernel; work
-// units in unit_of_f order.  (r01: before the converged-warp MMA issue this orientation was issue-bound at N = 160.)
+// SVD projection with a complex V on CTA pairs, frames on M (eq. 12): Z[f, r] = sum_kappa x16[f,kappa]
+// V16[r,kappa] (rows r < D_h -> Z_r, rows D_h + d -> Z_i, real-split [Re V | Im V] / [-Im V | Re V]).  A = this CTA's
+// 128 frames of X from the producer warps (produce_x_pair), B = proj_nt rows of V16 per pair tile (proj_nt/2 per CTA,
+// 2-SM TMA), N = proj_nt chosen at plan creation to cover the V rows tightly (cfg5: 2 x D_h = 384 -> 2 x 192).  The
+// accumulator lane is a frame and its columns are V rows, so each thread writes a contiguous segment of its frame's Z
+// row.  Warps as gemm2_kernel; work units in unit_of_f order.  (Real V plans use gemm2p_kernel.)
 // ================================================================================================================
-template <int Mi, int BPC, bool FOLD>
+template <int Mi, int BPC>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     gemm2f_kernel(const __grid_constant__ CUtensorMap tmV, GemmParams p) {
-    constexpr int kUnitsRaw = (BPC == 4) ? Mi * (Mi - 1) / 2 : (Mi * (Mi - 1) / 2 + 1) / 2;
-    constexpr int kU = (kUnitsRaw + 7) / 8 * 8;
-    constexpr bool kHalfPair = FOLD && (kU % 16 == 8);
-    constexpr int kSt = FOLD ? STAGES2 / 2 : STAGES2;       // FOLD: a stage holds a (Re, Im) slab pair
-    constexpr int kSP = FOLD ? 2 : 1;
-    constexpr int kAS = kSP * A2_BYTES, kBS = kSP * B2_BYTES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint8_t* sX = smem;                                     // A: 128 frames x 64 K per slab
-    uint8_t* sV = smem + kSt * kAS;                         // B: nt/2 V rows x 64 K per slab (<= 16 KB)
-    uint64_t* full = reinterpret_cast<uint64_t*>(sV + kSt * kBS);
-    uint64_t* empty = full + kSt;
-    uint64_t* tfull = empty + kSt;
+    uint8_t* sV = smem + STAGES2 * A2_BYTES;                // B: nt/2 V rows x 64 K per slab (<= 16 KB)
+    uint64_t* full = reinterpret_cast<uint64_t*>(sV + STAGES2 * B2_BYTES);
+    uint64_t* empty = full + STAGES2;
+    uint64_t* tfull = empty + STAGES2;
     uint64_t* tempty = tfull + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
@@ -807,7 +823,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     const uint32_t idesc = umma_idesc_f16(256, (uint32_t)nt);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < kSt; ++s) {
+        for (int s = 0; s < STAGES2; ++s) {
             mbar_init(&full[s], 1 + 2 * NPW2);              // leader's TMA (expect_tx) + producers of both CTAs
             mbar_init(&empty[s], 1);
         }
@@ -829,17 +845,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
         if (lane == 0) {
             int stage = 0;
             uint32_t phase = 0;
-            const uint32_t bytes = kSP * 2u * (uint32_t)hn * BK * 2;
+            const uint32_t bytes = 2u * (uint32_t)hn * BK * 2;
             for (int t = pair; t < units; t += n_pairs) {
                 const Unit w = unit_of_f(p, t);
-                for (int ks = w.k0; ks < w.k1; ks += kSP) {
+                for (int ks = w.k0; ks < w.k1; ++ks) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
-#pragma unroll
-                    for (int j = 0; j < kSP; ++j)
-                        tma_load_2d_2sm(sV + stage * kBS + j * B2_BYTES, &tmV, (ks + j) * BK, w.n * nt + (int)rank * hn,
-                                        &full[stage]);
-                    if (++stage == kSt) {
+                    tma_load_2d_2sm(sV + stage * B2_BYTES, &tmV, ks * BK, w.n * nt + (int)rank * hn, &full[stage]);
+                    if (++stage == STAGES2) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -857,54 +870,32 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                 const Unit w = unit_of_f(p, t);
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                int lp = 0;
-                const int n_lp = p.spc / 2;
-                for (int ks = w.k0; ks < w.k1; ks += kSP) {
+                for (int ks = w.k0; ks < w.k1; ++ks) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
-                    const uint64_t ad = adesc0 + (uint64_t)(stage * (kAS >> 4));
-                    const uint64_t bd = bdesc0 + (uint64_t)(stage * (kBS >> 4));
-                    if constexpr (FOLD) {
-                        const bool half = kHalfPair && lp == n_lp - 1;
-                        const uint32_t acc0 = ks != w.k0;
+                    const uint64_t ad = adesc0 + (uint64_t)(stage * (A2_BYTES >> 4));
+                    const uint64_t bd = bdesc0 + (uint64_t)(stage * (B2_BYTES >> 4));
+                    const uint32_t d_tmem = tmem_base + acc * BN;
+                    const uint32_t acc0 = ks != w.k0;
 #pragma unroll
-                        for (int part = 0; part < 2; ++part) {          // Re slab -> a (Z_r), Im slab -> b (Z_i)
-                            const uint32_t d_tmem = tmem_base + (uint32_t)part * BN;
-                            const uint64_t pa = ad + part * (A2_BYTES >> 4), pb = bd + part * (B2_BYTES >> 4);
-                            umma_f16_2sm_warp(d_tmem, pa, pb, idesc, acc0);
-                            umma_f16_2sm_warp(d_tmem, pa + 2, pb + 2, idesc, 1u);
-                            if (!half) {
-                                umma_f16_2sm_warp(d_tmem, pa + 4, pb + 4, idesc, 1u);
-                                umma_f16_2sm_warp(d_tmem, pa + 6, pb + 6, idesc, 1u);
-                            }
-                        }
-                        if (++lp == n_lp) lp = 0;
-                    } else {
-                        const uint32_t d_tmem = tmem_base + acc * BN;
-                        const uint32_t acc0 = ks != w.k0;
-#pragma unroll
-                        for (int kk = 0; kk < BK / 16; ++kk)
-                            umma_f16_2sm_warp(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, kk ? 1u : acc0);
-                    }
+                    for (int kk = 0; kk < BK / 16; ++kk)
+                        umma_f16_2sm_warp(d_tmem, ad + 2 * kk, bd + 2 * kk, idesc, kk ? 1u : acc0);
                     umma_commit_2sm_warp(&empty[stage], 0x3);
-                    if (++stage == kSt) {
+                    if (++stage == STAGES2) {
                         stage = 0;
                         phase ^= 1;
                     }
                 }
                 umma_commit_2sm_warp(&tfull[acc], 0x3);
-                if (FOLD) {
-                    acc_phase ^= 1;
-                } else if (++acc == 2) {
+                if (++acc == 2) {
                     acc = 0;
                     acc_phase ^= 1;
                 }
             }
         }
     } else if (warp < 6) {
-        // epilogue: TMEM lane = frame, columns = V rows [n*nt, n*nt + nt) -> Z[s][f][...]
+        // epilogue: TMEM lane = frame, columns = V rows [n*nt, n*nt + nt) -> Z[s][f][row] (row < 2*D_h)
         const int g = warp & 3;
-        const int half_z = p.ldz / 2;                       // D_h: Z_i columns start here
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = pair; t < units; t += n_pairs) {
@@ -915,39 +906,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
             float* zrow = p.Z + ((int64_t)w.s * p.F_pad + f) * p.ldz;
 #pragma unroll 1
             for (int j0 = 0; j0 < nt; j0 += 32) {
-                uint32_t r[32], rb[32];
+                uint32_t r[32];
                 tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + acc * BN + j0, r);
-                if (FOLD) tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + BN + j0, rb);
                 tmem_ld_wait();
-                const int r0 = w.n * nt + j0;               // first V row (FOLD: d) of these 32 columns
-                if (f < p.F) {
-                    if (FOLD) {
-                        if (r0 < half_z) {                  // whole 32-row group inside [0, D_h): D_h % 64 == 0
-                            float4* za = reinterpret_cast<float4*>(zrow + r0);
-                            float4* zb = reinterpret_cast<float4*>(zrow + half_z + r0);
+                const int r0 = w.n * nt + j0;               // first V row of these 32 columns
+                if (f < p.F && r0 < p.ldz) {
+                    float4* z = reinterpret_cast<float4*>(zrow + r0);
 #pragma unroll
-                            for (int q = 0; q < 8; ++q) {
-                                za[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                                                    __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-                                zb[q] = make_float4(__uint_as_float(rb[4 * q]), __uint_as_float(rb[4 * q + 1]),
-                                                    __uint_as_float(rb[4 * q + 2]), __uint_as_float(rb[4 * q + 3]));
-                            }
-                        }
-                    } else if (r0 < p.ldz) {
-                        float4* z = reinterpret_cast<float4*>(zrow + r0);
-#pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            z[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
-                                               __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
-                    }
+                    for (int q = 0; q < 8; ++q)
+                        z[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                           __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive_cluster(&tempty[acc], 0);
-            if (FOLD) {
-                acc_phase ^= 1;
-            } else if (++acc == 2) {
+            if (++acc == 2) {
                 acc = 0;
                 acc_phase ^= 1;
             }
@@ -961,8 +935,280 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
         for (int t = pair; t < units; t += n_pairs) {
             const Unit w = unit_of_f(p, t);
             const int f = w.m * 256 + (int)rank * 128 + tp;
-            produce_x_pair<Mi, BPC, kSt, kAS, FOLD, A2_BYTES>(p, w, f, f < p.F, sX, full, empty, stage, phase,
-                                                              row_off, xr);
+            produce_x_pair<Mi, BPC, STAGES2, A2_BYTES>(p, w, f, f < p.F, sX, full, empty, stage, phase, row_off, xr);
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    if (warp == 0) {
+        tc_fence_after();
+        tmem_dealloc_2sm<512>(tmem_base);
+    }
+}
+
+// ================================================================================================================
+// SVD projection with a real V (R22) on CTA pairs, "part rows" (eq. 12): Z_r = V^T x_r and
+// Z_i = V^T x_i share V, so the A operand carries the two parts of a frame as two rows — CTA r of the pair: rows
+// [0,64) = Re x of frames [m*128 + 64r, +64), rows [64,128) = Im x of the same frames — and B = V16 in the part layout
+// (one copy of V per K position, Plan::K_P) holds all nt <= 512 V rows of the tile in one accumulator of nt TMEM
+// columns (n_mma = ceil(nt/256) MMAs of nmma columns per K step).  X is produced once per frame tile for all V rows
+// (gemm2f_kernel, 256-column tiles, produced it once per V tile and was producer-bound at N = 160), and each V slab
+// is staged once.  One accumulator (<= 512 columns): the epilogue is not overlapped with the next tile's MMAs.
+// Warps: 0 TMA (+TMEM alloc), 1 MMA (leader), 2-5 epilogue (lane groups 2,3,0,1), 6-7 producers of the Re rows,
+// 8-9 producers of the Im rows.  Work units in unit_of_f order (split slowest, V tile, frame tile fastest).
+// ================================================================================================================
+constexpr int P_A_BYTES = 128 * BK * 2;                // 16 KB: this CTA's 128 A rows (64 frames x {Re, Im})
+constexpr int P_MAX_STAGES = 8;
+
+// Producer warps of gemm2p_kernel: this thread's A row (PART 0: Re x, PART 1: Im x of frame f, eqs. 3, 7) for the bin
+// chunks [w.c0, w.c1), one 16-unit slab per stage (the last slab of a chunk holds kU % 16 units when that is 8).
+template <int Mi, int BPC, int PART>
+__device__ __forceinline__ void produce_x_part(const GemmParams& p, const Unit& w, int f, bool valid, uint8_t* smem,
+                                               uint64_t* full, uint64_t* empty, int& stage, uint32_t& phase,
+                                               uint32_t row_off, uint32_t xr) {
+    constexpr PairTab<Mi> PT{};
+    constexpr int kPairs = Mi * (Mi - 1) / 2;
+    constexpr int kUnitsRaw = (BPC == 4) ? kPairs : (kPairs + 1) / 2;
+    constexpr int kU = (kUnitsRaw + 7) / 8 * 8;
+    constexpr int kUB = BPC * 4;
+    const int lane = threadIdx.x & 31;
+    uint32_t e[Mi][BPC];
+    auto load_rec = [&](int m, const uint8_t* base) {
+        if constexpr (BPC == 4) {
+            const uint4 v = valid ? __ldg(reinterpret_cast<const uint4*>(base + (int64_t)m * p.F_pad * kUB))
+                                  : make_uint4(0, 0, 0, 0);
+            e[m][0] = v.x;
+            e[m][1] = v.y;
+            e[m][2] = v.z;
+            e[m][3] = v.w;
+        } else {
+            const uint2 v = valid ? __ldg(reinterpret_cast<const uint2*>(base + (int64_t)m * p.F_pad * kUB))
+                                  : make_uint2(0, 0);
+            e[m][0] = v.x;
+            e[m][1] = v.y;
+        }
+    };
+    if (w.c0 < w.c1) {
+        const uint8_t* src0 = p.P16 + ((int64_t)w.c0 * Mi * p.F_pad + f) * kUB;
+#pragma unroll
+        for (int m = 0; m < Mi; ++m) load_rec(m, src0);
+    }
+#pragma unroll 1
+    for (int c = w.c0; c < w.c1; ++c) {
+        const uint8_t* src = p.P16 + ((int64_t)c * Mi * p.F_pad + f) * kUB;
+        const uint8_t* nxt = src + (int64_t)Mi * p.F_pad * kUB;
+        const bool more = c + 1 < w.c1;
+        if constexpr (BPC != 4) {
+            if (c != w.c0) {
+#pragma unroll
+                for (int m = 0; m < Mi; ++m) load_rec(m, src);
+            }
+        }
+        if (p.prefetch && valid && more) {
+#pragma unroll
+            for (int m = 0; m < Mi; ++m)
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(nxt + (int64_t)m * p.F_pad * kUB));
+        }
+        uint32_t pend0 = 0u, pend1 = 0u;
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            if ((u & 15) == 0) mbar_wait(&empty[stage], phase ^ 1);
+            // this part's two words of unit u: BPC 4 -> bins k0k1, k2k3 of pair u; BPC 2 -> bins k0k1 of pairs 2u, 2u+1
+            uint32_t w0 = 0u, w1 = 0u;
+            if constexpr (BPC == 4) {
+                if (u < kPairs) {
+                    const int a = PT.i[u], b = PT.j[u];
+                    if (PART == 0) {           // Re x = ra rb + ia ib   (eq. 3)
+                        w0 = h2fma(e[a][0], e[b][0], h2mul(e[a][2], e[b][2]));
+                        w1 = h2fma(e[a][1], e[b][1], h2mul(e[a][3], e[b][3]));
+                    } else {                   // Im x = ia rb - ra ib
+                        w0 = h2fma(e[a][2], e[b][0], h2mul(e[a][0] ^ 0x80008000u, e[b][2]));
+                        w1 = h2fma(e[a][3], e[b][1], h2mul(e[a][1] ^ 0x80008000u, e[b][3]));
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+                    const int pp = 2 * u + h;
+                    uint32_t v = 0u;
+                    if (pp < kPairs) {
+                        const int a = PT.i[pp], b = PT.j[pp];
+                        v = PART == 0 ? h2fma(e[a][0], e[b][0], h2mul(e[a][1], e[b][1]))
+                                      : h2fma(e[a][1], e[b][0], h2mul(e[a][0] ^ 0x80008000u, e[b][1]));
+                    }
+                    if (h == 0) w0 = v; else w1 = v;
+                }
+            }
+            if constexpr (BPC == 4) {
+#pragma unroll
+                for (int m = 0; m < Mi; ++m)
+                    if (PT.last[m] == u && more) load_rec(m, nxt);
+            }
+            if ((u & 1) == 0) {
+                pend0 = w0;
+                pend1 = w1;
+            } else {                           // units 2j, 2j+1 -> 16-byte chunk j of the slab row (swizzled)
+                const uint32_t pos = row_off + (((((uint32_t)u & 15u) >> 1) ^ xr) << 4);
+                st_shared_v4(smem_u32(smem + stage * p.stage_bytes) + pos, pend0, pend1, w0, w1);
+            }
+            if ((u & 15) == 15 || u == kU - 1) {
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive_cluster(&full[stage], 0);   // the leader's barrier
+                if (++stage == p.stages) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    }
+}
+
+template <int Mi, int BPC>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
+    gemm2p_kernel(const __grid_constant__ CUtensorMap tmV, GemmParams p) {
+    constexpr int kUnitsRaw = (BPC == 4) ? Mi * (Mi - 1) / 2 : (Mi * (Mi - 1) / 2 + 1) / 2;
+    constexpr int kU = (kUnitsRaw + 7) / 8 * 8;
+    constexpr bool kHalf = (kU % 16 == 8);                  // the last slab of a chunk holds 8 units: K = 32
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // stage s: [A: 128 rows x 128 B][B: nt/2 V rows x 128 B, as n_mma blocks of nmma/2 rows]
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * p.stage_bytes);
+    uint64_t* empty = full + P_MAX_STAGES;
+    uint64_t* tfull = empty + P_MAX_STAGES;
+    uint64_t* tempty = tfull + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 1);
+
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+    const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
+    const int units = p.m_tiles * p.n_tiles * p.ksplit;
+    const int nt = p.bn, hm = p.nmma / 2;                  // V rows per tile / per CTA per MMA
+    const uint32_t idesc = umma_idesc_f16(256, (uint32_t)p.nmma);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < p.stages; ++s) {
+            mbar_init(&full[s], 1 + 2 * NPW2);              // leader's TMA (expect_tx) + producers of both CTAs
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(tfull, 1);
+        mbar_init(tempty, 8);
+        fence_mbar_init();
+    }
+    if (warp == 0) tmem_alloc_2sm<512>(tmem_slot);
+    if (warp == 1 && lane == 0) tma_prefetch_desc(&tmV);
+    tc_fence_before();
+    __syncthreads();
+    cluster_sync();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0) {
+        if (lane == 0) {
+            int stage = 0;
+            uint32_t phase = 0;
+            const uint32_t bytes = (uint32_t)nt * BK * 2;     // both CTAs' nt/2 rows x 128 B
+            for (int t = pair; t < units; t += n_pairs) {
+                const Unit w = unit_of_f(p, t);
+                for (int ks = w.k0; ks < w.k1; ++ks) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
+                    uint8_t* sB = smem + stage * p.stage_bytes + P_A_BYTES;
+                    for (int j = 0; j < p.n_mma; ++j)
+                        tma_load_2d_2sm(sB + j * hm * (BK * 2), &tmV, ks * BK, w.n * nt + j * p.nmma + (int)rank * hm,
+                                        &full[stage]);
+                    if (++stage == p.stages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (leader) {                                       // converged-warp MMA issue (see gemm2_kernel)
+            const uint64_t desc0 = umma_desc_sw128(smem_u32(smem));
+            const uint64_t sdesc = (uint64_t)(p.stage_bytes >> 4), bdesc = (uint64_t)(P_A_BYTES >> 4);
+            const uint64_t jdesc = (uint64_t)((hm * BK * 2) >> 4);
+            int stage = 0;
+            uint32_t phase = 0, acc_phase = 0;
+            for (int t = pair; t < units; t += n_pairs) {
+                const Unit w = unit_of_f(p, t);
+                mbar_wait(tempty, acc_phase ^ 1);
+                tc_fence_after();
+                int lp = 0;                                 // slab within the bin chunk
+                for (int ks = w.k0; ks < w.k1; ++ks) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint64_t ad = desc0 + (uint64_t)stage * sdesc;
+                    const bool half = kHalf && lp == p.spc - 1;
+                    const uint32_t acc0 = ks != w.k0;
+                    for (int j = 0; j < p.n_mma; ++j) {
+                        const uint32_t d_tmem = tmem_base + (uint32_t)(j * p.nmma);
+                        const uint64_t bd = ad + bdesc + (uint64_t)j * jdesc;
+                        umma_f16_2sm_warp(d_tmem, ad, bd, idesc, acc0);
+                        umma_f16_2sm_warp(d_tmem, ad + 2, bd + 2, idesc, 1u);
+                        if (!half) {
+                            umma_f16_2sm_warp(d_tmem, ad + 4, bd + 4, idesc, 1u);
+                            umma_f16_2sm_warp(d_tmem, ad + 6, bd + 6, idesc, 1u);
+                        }
+                    }
+                    umma_commit_2sm_warp(&empty[stage], 0x3);
+                    if (++stage == p.stages) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                    if (++lp == p.spc) lp = 0;
+                }
+                umma_commit_2sm_warp(tfull, 0x3);
+                acc_phase ^= 1;
+            }
+        }
+    } else if (warp < 6) {
+        // epilogue: TMEM lane = A row (part g/2, frame (g&1)*32 + lane), columns = V rows [n*nt, n*nt + nt) -> Z
+        const int g = warp & 3;
+        const int part = g >> 1;
+        uint32_t acc_phase = 0;
+        for (int t = pair; t < units; t += n_pairs) {
+            const Unit w = unit_of_f(p, t);
+            mbar_wait(tfull, acc_phase);
+            tc_fence_after();
+            const int f = w.m * 128 + (int)rank * 64 + (g & 1) * 32 + lane;
+            float* zrow = p.Z + ((int64_t)w.s * p.F_pad + f) * p.ldz + part * p.zh + w.n * nt;
+#pragma unroll 1
+            for (int j0 = 0; j0 < nt; j0 += 32) {
+                uint32_t r[32];
+                tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + j0, r);
+                tmem_ld_wait();
+                if (f < p.F) {
+                    float4* z = reinterpret_cast<float4*>(zrow + j0);
+#pragma unroll
+                    for (int q = 0; q < 8; ++q)
+                        z[q] = make_float4(__uint_as_float(r[4 * q]), __uint_as_float(r[4 * q + 1]),
+                                           __uint_as_float(r[4 * q + 2]), __uint_as_float(r[4 * q + 3]));
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive_cluster(tempty, 0);
+            acc_phase ^= 1;
+        }
+    } else {
+        const int tp = (warp - 6) * 32 + lane;              // A row of this CTA: 0..63 Re part, 64..127 Im part
+        const uint32_t row_off = (uint32_t)((tp >> 3) * 1024 + (tp & 7) * 128);
+        const uint32_t xr = (uint32_t)(tp & 7);
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int t = pair; t < units; t += n_pairs) {
+            const Unit w = unit_of_f(p, t);
+            const int f = w.m * 128 + (int)rank * 64 + (tp & 63);
+            if (tp < 64)
+                produce_x_part<Mi, BPC, 0>(p, w, f, f < p.F, smem, full, empty, stage, phase, row_off, xr);
+            else
+                produce_x_part<Mi, BPC, 1>(p, w, f, f < p.F, smem, full, empty, stage, phase, row_off, xr);
         }
     }
 
@@ -991,8 +1237,8 @@ static cudaError_t set_attr_pair() {
     if ((e = cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, 1, false>, attr, sm))) return e;
     if ((e = cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, 0, true>, attr, sm))) return e;
     if ((e = cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, 1, true>, attr, sm))) return e;
-    if ((e = cudaFuncSetAttribute(gemm2f_kernel<Mi, BPC, false>, attr, sm))) return e;
-    return cudaFuncSetAttribute(gemm2f_kernel<Mi, BPC, true>, attr, sm);
+    if ((e = cudaFuncSetAttribute(gemm2f_kernel<Mi, BPC>, attr, sm))) return e;
+    return cudaFuncSetAttribute(gemm2p_kernel<Mi, BPC>, attr, 227 * 1024);
 }
 
 cudaError_t gemm_set_attributes() {
@@ -1044,13 +1290,13 @@ static cudaError_t launch_one(const CUtensorMap& A, const CUtensorMap& B, const 
 ProjShape proj_shape(const Plan& p, const Band& b, int F) {
     ProjShape sh;
     sh.pair = p.pair_proj;
-    const int f_tiles = (F + BN - 1) / BN;
+    const int f_tiles = p.svd_fold && p.pair_proj ? (F + 127) / 128 : (F + BN - 1) / BN;   // part kernel: 128 frames
     sh.m_tiles = sh.pair ? f_tiles : (2 * p.Dh) / BM;
     sh.n_tiles = sh.pair ? p.proj_ntiles : f_tiles;
     const int units = sh.m_tiles * sh.n_tiles;
     const int slots = sh.pair ? p.num_sms / 2 : p.num_sms;
     const int nc = b.c_hi - b.c_lo;
-    const double slabs = (double)nc * (p.svd_fold ? p.spc_F : p.L.U / 8);
+    const double slabs = (double)nc * (p.svd_fold ? p.spc_P : p.L.U / 8) * (p.svd_fold ? p.proj_nmma : 1);
     double best_t = 1e300;
     sh.ksplit = 1;
     constexpr double fixed = 24.0;            // per-unit fixed cost in slabs (pipeline fill + epilogue), r01 fit
@@ -1100,7 +1346,7 @@ cudaError_t launch_gemm(const Plan& p, const Band& b, int mode, int F, cudaStrea
     gp.n_tiles = (F + BN - 1) / BN;
     gp.keys = p.d_keys;
     gp.Z = p.d_Z32;
-    gp.ldz = 2 * p.Dh;
+    gp.ldz = 2 * p.Zh;
     gp.ksplit = 1;
     gp.spc = srp_mode ? p.spc_W : p.L.U / 8;
     gp.bn = BN;
@@ -1116,15 +1362,9 @@ cudaError_t launch_gemm(const Plan& p, const Band& b, int mode, int F, cudaStrea
         gp.rows_valid = p.fold ? p.fold_rows : p.Q_eff;
         gp.m_tiles = p.W_rows / (p.pair_srp ? 256 : BM);
     } else if (mode == 1) {
-        A = &p.tm_V;
-        if (p.svd_fold) {              // real V: fold rows d, accumulators a -> Z_r (column d), b -> Z_i (Dh + d)
-            gp.n_slabs = (int)(p.K_F / BK);
-            gp.spc = p.spc_F;
-            gp.rows_valid = p.D;
-        } else {
-            gp.n_slabs = (int)(p.L.K_total / BK);
-            gp.rows_valid = 2 * p.Dh;
-        }
+        A = &p.tm_V;                   // complex V (the real-V part kernel sets its own shape below)
+        gp.n_slabs = (int)(p.L.K_total / BK);
+        gp.rows_valid = 2 * p.Dh;
         gp.m_tiles = (2 * p.Dh) / BM;
     } else {                           // 2: SVD search + argmax; 4: its power map Re{Dhat Zhat}[f][class] -> S
         A = &p.tm_R;
@@ -1133,7 +1373,9 @@ cudaError_t launch_gemm(const Plan& p, const Band& b, int mode, int F, cudaStrea
         gp.m_tiles = p.Q_pad / BM;
         gp.rows_valid = p.Q_eff;
         if (mode == 2) {
-            gp.keys = p.d_keys + p.F_pad;
+            gp.keys = p.d_keys + 2 * p.F_pad;                 // FP16 keys; the rescore writes the SVD keys
+            gp.cand = p.d_cand;
+            gp.ccnt = p.d_ccnt;
         } else {
             gp.Z = p.d_S;
             gp.ldz = p.Q_pad;
@@ -1152,7 +1394,36 @@ cudaError_t launch_gemm(const Plan& p, const Band& b, int mode, int F, cudaStrea
         // split K (at chunk boundaries) to fill the SMs, deterministic partial buffers
         const ProjShape sh = proj_shape(p, b, F);
         gp.ksplit = sh.ksplit;
-        if (sh.pair) {                 // frames on M, V rows on N (gemm2f_kernel)
+        if (sh.pair && p.svd_fold) {   // real V: part rows (gemm2p_kernel), all V rows of a tile in one accumulator
+            gp.m_tiles = sh.m_tiles;
+            gp.n_tiles = sh.n_tiles;
+            gp.bn = p.proj_nt;
+            gp.spc = p.spc_P;
+            gp.n_slabs = (int)(p.K_P / BK);
+            gp.n_mma = p.proj_nmma;
+            gp.nmma = p.proj_nt / p.proj_nmma;
+            gp.ldz = 2 * p.Zh;
+            gp.zh = p.Zh;
+            gp.stage_bytes = P_A_BYTES + (p.proj_nt / 2) * BK * 2;
+            gp.stages = (227 * 1024 - 1024 - 256) / gp.stage_bytes;
+            gp.stages = gp.stages > P_MAX_STAGES ? P_MAX_STAGES : gp.stages;
+            const int units = gp.m_tiles * gp.n_tiles * gp.ksplit;
+            if (units == 0) return cudaSuccess;
+            const int pairs = units < npairs ? units : npairs;
+            const size_t smem = 1024 + (size_t)gp.stages * gp.stage_bytes + 256;
+#define SVD_PROJP(MI, BP)                                                                                        \
+    if (p.L.Mi == MI) {                                                                                         \
+        gemm2p_kernel<MI, BP><<<2 * pairs, THREADS2, smem, s>>>(*A, gp);                                        \
+        return cudaGetLastError();                                                                              \
+    }
+            SVD_PROJP(4, 4)
+            SVD_PROJP(8, 4)
+            SVD_PROJP(16, 4)
+            SVD_PROJP(32, 2)
+#undef SVD_PROJP
+            return cudaErrorInvalidValue;
+        }
+        if (sh.pair) {                 // complex V: frames on M, V rows on N (gemm2f_kernel)
             gp.m_tiles = sh.m_tiles;
             gp.n_tiles = sh.n_tiles;
             gp.bn = p.proj_nt;
@@ -1161,10 +1432,7 @@ cudaError_t launch_gemm(const Plan& p, const Band& b, int mode, int F, cudaStrea
             const int pairs = units < npairs ? units : npairs;
 #define SVD_PROJ(MI, BP)                                                                                         \
     if (p.L.Mi == MI) {                                                                                         \
-        if (p.svd_fold)                                                                                         \
-            gemm2f_kernel<MI, BP, true><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(*A, gp);                      \
-        else                                                                                                    \
-            gemm2f_kernel<MI, BP, false><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(*A, gp);                     \
+        gemm2f_kernel<MI, BP><<<2 * pairs, THREADS2, SMEM2_BYTES, s>>>(*A, gp);                                 \
         return cudaGetLastError();                                                                              \
     }
             SVD_PROJ(4, 4)

@@ -68,25 +68,35 @@ struct Plan {
     std::vector<int> rb_cls, rb_partner, rb_kind;   // real basis row i: class, antipode (-1), kind 0 Re / 1 Im / 2 real
     int64_t K_W = 0;              // contraction length of W16
     int spc_W = 0;                // W16 slabs per bin chunk
-    __half* d_V16 = nullptr;      // [V_rows][K_total], or [V_rows][K_F] folded (svd_fold: one row per d)
-    __half* d_R16 = nullptr;      // [Q_pad][K2]
+    __half* d_V16 = nullptr;      // [V_rows][K_total] (complex V), or [V_rows][K_P] part layout (svd_fold)
+    // part layout (real V, gemm2p): the projection's A rows carry Re x and Im x of a frame separately, so V is stored
+    // once per K position: per chunk SP = ceil(U/16) slabs, unit u's 4 values at (c*SP + u/16)*64 + (u%16)*4
+    int64_t K_P = 0;
+    int spc_P = 0;
+    __half* d_R16 = nullptr;      // [Q_pad][K2]   FP16 normalised dictionary rows [Re | -Im] (search GEMM)
+    float* d_R32 = nullptr;       // [Q_eff][K2]   the same in FP32 (exact rescore of the search candidates)
     int* d_rep = nullptr;         // [Q_eff]
     float* d_delay = nullptr;     // [Q][M]  relative arrival delays (samples)
     float* d_window = nullptr;    // [N]
     float2* d_twN = nullptr;      // [N]     e^{-j 2 pi k / N}
     // workspace
     uint8_t* d_P16 = nullptr;     // phasors
-    unsigned long long* d_keys = nullptr;  // [2][F_pad]: SRP keys, SVD search keys
-    float* d_Z32 = nullptr;       // [zsplit_max][F_pad][2*Dh] partial Z of the split-K projection
+    unsigned long long* d_keys = nullptr;  // [3][F_pad]: SRP keys, SVD keys (rescored), SVD FP16 search keys
+    float* d_Z32 = nullptr;       // [zsplit_max][F_pad][2*Zh] partial Z of the split-K projection (Z_r | Z_i)
+    int Zh = 0;                   // half width of a Z32 row: >= D_h and >= the projection's V rows
+    float* d_Zn32 = nullptr;      // [F_pad][K2] FP32 Zhat = Z/||Z|| [Re | Im] (rescore)
+    unsigned long long* d_cand = nullptr;  // [F_pad][SEARCH_CAP] search candidates (FP16 score, class)
+    int* d_ccnt = nullptr;        // [F_pad] candidates per frame
     int V_rows = 0;               // rows of V16: proj_ntiles * proj_nt (pair projection) or 2*Dh (1-CTA)
     int proj_nt = 0;              // V rows per pair tile of the frames-on-M projection (multiple of 32, <= 256)
     int proj_ntiles = 0;          // V row tiles
+    int proj_nmma = 1;            // MMAs per K step of a part-kernel tile (proj_nt > 256 -> 2 of proj_nt/2 columns)
     bool pair_proj = true;
     int zsplit_max = 1;
     // small batches: SRP as split-K partial power maps + sum/argmax (the argmax epilogue cannot split K)
     float* d_Ypart = nullptr;     // [srp_split_max][F_pad][Q_pad]
     int srp_split_max = 0;
-    __half* d_Zs16 = nullptr;     // [F_pad][K2]
+    __half* d_Zs16 = nullptr;     // [F_pad][K2] FP16 Zhat [Re | Im] (search GEMM operand)
     int* d_zflag = nullptr;       // [F_pad]
     // multi-source (top-k) workspace, allocated on first use: power map S[F_pad][Q_pad], class lists [F_pad][4]
     float* d_S = nullptr;
@@ -167,6 +177,13 @@ cudaError_t launch_zsplit(const Plan& p, const Band& b, int F, cudaStream_t s, b
 int srp_split_ways(const Plan& p, const Band& b, int F);   // > 1: the SRP call takes the small-batch split-K path
 cudaError_t launch_split_argmax(const Plan& p, int F, int S, cudaStream_t s);
 constexpr int MAX_KSPLIT = 32;               // cap on K splits (chunk ranges) of the store-mode GEMMs
+// FP16 search + exact rescore: a row enters a frame's candidate list when its FP16 score is within SEARCH_TAU of the
+// frame's running FP16 maximum.  SEARCH_TAU = 2.5e-3 >= twice the FP16 error bound of a unit-vector dot product
+// (2^-10 + FP32 accumulation), so the exact argmax is always a candidate; lists longer than SEARCH_CAP fall back to
+// an exact scan of every class for that frame.
+constexpr int SEARCH_CAP = 32;
+constexpr float SEARCH_TAU = 2.5e-3f;
+cudaError_t launch_rescore(const Plan& p, int F, cudaStream_t s);
 struct ProjShape {
     bool pair;
     int m_tiles, n_tiles, ksplit;   // pair: m = 256-frame tiles, n = proj_nt-row V tiles; 1-CTA: m = 128-row V tiles

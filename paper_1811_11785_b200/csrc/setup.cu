@@ -9,7 +9,8 @@
 //          Twin classes (bitwise-identical rows, R11) enter with multiplicity n_c:  G' = N^1/2 G_r N^1/2
 //          has the spectrum of the full W W^H.  Rank D by eq. 11 with Tr{W W^H} = Q P Kb exactly.
 //          V_D = W^H U_D S_D^{-1} (eq. 10) formed column-chunk-wise with cuBLAS ZGEMM on generated W chunks.
-//          Dictionary rows D_q = (U S)_q (eq. 13) normalised -> split FP16 [hi | lo | hi].
+//          Dictionary rows D_q = (U S)_q (eq. 13) normalised -> FP16 [Re | -Im] for the search GEMM
+//          and FP32 for the exact rescore of its candidates.
 #include <cublas_v2.h>
 #include <cuComplex.h>
 #include <cuda_fp16.h>
@@ -233,9 +234,10 @@ __global__ void rwchunk_kernel(const double* __restrict__ tau, const int* __rest
     Wc[(int64_t)cc * n + i] = kind == 0 ? r2 * cs : (kind == 1 ? r2 * sn : cs);
 }
 
-// real V chunk (column-major C x D) -> folded V16 row d: the same value in the Re slab (-> Z_r) and the Im slab (-> Z_i)
-__global__ void pack_v16f_kernel(const double* __restrict__ Vc, int C, int64_t c0, int M, int Mi, int Kb, int bpc,
-                                 int SP, int64_t K_F, double scale, __half* __restrict__ V16) {
+// real V chunk -> "part" V16 row d (svd_part: the projection's A rows carry Re x and Im x of a frame separately, so V is
+// stored once per K position): unit u of chunk c, value s at (c*SP + u/16)*64 + (u%16)*4 + s
+__global__ void pack_v16p_kernel(const double* __restrict__ Vc, int C, int64_t c0, int M, int Mi, int Kb, int bpc,
+                                 int SP, int64_t K_P, double scale, __half* __restrict__ V16) {
     const int cc = blockIdx.x * blockDim.x + threadIdx.x;
     const int d = blockIdx.y;
     if (cc >= C) return;
@@ -247,10 +249,11 @@ __global__ void pack_v16f_kernel(const double* __restrict__ Vc, int C, int64_t c
         ++i;
     }
     const int pi = pair_index(i, i + 1 + rem, Mi);
-    const __half v = __double2half(scale * Vc[(int64_t)d * C + cc]);
-    __half* row = V16 + (int64_t)d * K_F;
-    row[kappa_fold(pi, k, 0, bpc, SP)] = v;
-    row[kappa_fold(pi, k, 1, bpc, SP)] = v;
+    const int c = k / bpc;
+    const int u = (bpc == 4) ? pi : (pi >> 1);
+    const int sl = (bpc == 4) ? (k % 4) : ((pi & 1) * 2 + k % 2);
+    V16[(int64_t)d * K_P + ((int64_t)c * SP + u / 16) * 64 + (u % 16) * 4 + sl] =
+        __double2half(scale * Vc[(int64_t)d * C + cc]);
 }
 
 // class-basis eigenvectors U' = T^H U~ (columns jd >= n - D) into the complex n x n buffer read by pack_r16_kernel:
@@ -272,9 +275,10 @@ __global__ void ucplx_kernel(const double* __restrict__ Ur, const int* __restric
     }
 }
 
-// R16 row a: Rhat_a = normalise(U'[a][jd] sqrt(lambda_d)) -> [hi(Re) hi(-Im) | lo(Re) lo(-Im) | hi(Re) hi(-Im)]
+// Row a of the dictionary: Rhat_a = normalise(U'[a][jd] sqrt(lambda_d)) -> R16 FP16 [Re | -Im] (search GEMM) and R32
+// FP32 [Re | -Im] (exact rescore of the search candidates)
 __global__ void pack_r16_kernel(const cuDoubleComplex* __restrict__ Uv, const double* __restrict__ lam, int n, int D,
-                                int Dh, int K2, __half* __restrict__ R16) {
+                                int Dh, int K2, __half* __restrict__ R16, float* __restrict__ R32) {
     const int a = blockIdx.x;
     __shared__ double red[32];
     double ss = 0.0;
@@ -294,20 +298,16 @@ __global__ void pack_r16_kernel(const cuDoubleComplex* __restrict__ Uv, const do
     __syncthreads();
     const double inv = 1.0 / sqrt(red[0]);
     __half* row = R16 + (int64_t)a * K2;
-    const int W2 = 2 * Dh;
+    float* row32 = R32 + (int64_t)a * K2;
     for (int d = threadIdx.x; d < D; d += blockDim.x) {
         const int jd = n - 1 - d;
         const cuDoubleComplex u = Uv[(int64_t)jd * n + a];
         const double sl = sqrt(lam[jd]) * inv;
         const float vr = (float)(u.x * sl), vi = (float)(-u.y * sl);  // [Re R | -Im R]
-        const __half hr = __float2half_rn(vr), hi = __float2half_rn(vi);
-        const __half lr = __float2half_rn(vr - __half2float(hr)), li = __float2half_rn(vi - __half2float(hi));
-        row[d] = hr;
-        row[Dh + d] = hi;
-        row[W2 + d] = lr;
-        row[W2 + Dh + d] = li;
-        row[2 * W2 + d] = hr;
-        row[2 * W2 + Dh + d] = hi;
+        row[d] = __float2half_rn(vr);
+        row[Dh + d] = __float2half_rn(vi);
+        row32[d] = vr;
+        row32[Dh + d] = vi;
     }
 }
 
@@ -331,16 +331,20 @@ svdphat_status setup_srp_operand(Plan& p, const double* d_tau_cls) {
     return SVDPHAT_OK;
 }
 
-// V row tiling of the frames-on-M pair projection: the fewest tiles of <= 256 rows (multiples of 32) covering `rows`.
-// cfg3: real V, D = 318 -> 2 x 160; complex V, 2*D_h = 640 -> 3 x 224.
+// V row tiling of the frames-on-M pair projections: the fewest tiles covering `rows`, each a multiple of 32 rows and at
+// most 256 (complex V, gemm2f: one MMA of N <= 256 per K step) or 512 (real V "part" kernel gemm2p: one accumulator of
+// <= 512 TMEM columns, ceil(nt/256) MMAs per K step).  cfg3: real V, D = 318 (+2 SRP tail rows) -> 1 x 320; complex
+// V, 2*D_h = 640 -> 3 x 224.
 static void choose_proj_tiles(Plan& p, int rows) {
     if (!p.pair_proj) {
         p.V_rows = rows;
         return;
     }
-    p.proj_ntiles = (rows + 255) / 256;
+    const int cap = p.svd_fold ? 512 : 256;
+    p.proj_ntiles = (rows + cap - 1) / cap;
     p.proj_nt = ((rows + p.proj_ntiles - 1) / p.proj_ntiles + 31) / 32 * 32;
     p.V_rows = p.proj_ntiles * p.proj_nt;
+    p.proj_nmma = p.proj_nt > 256 ? 2 : 1;
 }
 
 namespace {
@@ -363,8 +367,8 @@ static svdphat_status setup_real_v(Plan& p, const double* d_tau_cls, int n, int 
         rbmat_kernel<<<grid, 128>>>(Ur, lam, cnt, d_rb, n, D, (double*)B.ptr);
         SVD_CUDA_TRY(cudaGetLastError());
     }
-    choose_proj_tiles(p, D);
-    p.bytes_V = (int64_t)p.V_rows * p.K_F * 2;
+    choose_proj_tiles(p, D + 2 * p.tail_n);                 // + the SRP tail rows (a Re row and an Im row each)
+    p.bytes_V = (int64_t)p.V_rows * p.K_P * 2;
     SVD_CUDA_TRY(cudaMalloc(&p.d_V16, p.bytes_V));
     SVD_CUDA_TRY(cudaMemset(p.d_V16, 0, p.bytes_V));
     int64_t CH = std::max<int64_t>(256, std::min<int64_t>(p.PK, (int64_t)(1ll << 30) / ((int64_t)n * 8)));
@@ -390,7 +394,7 @@ static svdphat_status setup_real_v(Plan& p, const double* d_tau_cls, int n, int 
             return SVDPHAT_CUDA;
         }
         dim3 g2(cdiv(C, 128), D);
-        pack_v16f_kernel<<<g2, 128>>>((const double*)Vc.ptr, C, c0, p.M, p.L.Mi, p.Kb, p.L.bpc, p.spc_F / 2, p.K_F,
+        pack_v16p_kernel<<<g2, 128>>>((const double*)Vc.ptr, C, c0, p.M, p.L.Mi, p.Kb, p.L.bpc, p.spc_P, p.K_P,
                                       scale, p.d_V16);
     }
     cublasDestroy(bh);
@@ -522,7 +526,7 @@ svdphat_status setup_svd_operands(Plan& p, const double* d_tau_cls, int rank_D) 
     for (int i = 0; i < D; ++i) kept += p.sigma2[i];
     p.energy_kept = kept / p.trace;
     p.Dh = (D + 63) / 64 * 64;
-    p.K2 = 3 * 2 * p.Dh;
+    p.K2 = 2 * p.Dh;
 
     if (p.svd_fold) {
         svdphat_status st = setup_real_v(p, d_tau_cls, n, D, (const double*)Gr.ptr, (const double*)lam.ptr,
@@ -571,10 +575,13 @@ svdphat_status setup_svd_operands(Plan& p, const double* d_tau_cls, int rank_D) 
         SVD_CUDA_TRY(cudaGetLastError());
     }
     // ---- normalised dictionary rows (split FP16)
-    p.bytes_R = (int64_t)p.Q_pad * p.K2 * 2;
-    SVD_CUDA_TRY(cudaMalloc(&p.d_R16, p.bytes_R));
-    SVD_CUDA_TRY(cudaMemset(p.d_R16, 0, p.bytes_R));
-    pack_r16_kernel<<<n, 256>>>((const cuDoubleComplex*)G.ptr, (const double*)lam.ptr, n, D, p.Dh, p.K2, p.d_R16);
+    p.bytes_R = (int64_t)p.Q_pad * p.K2 * 2 + (int64_t)n * p.K2 * 4;
+    SVD_CUDA_TRY(cudaMalloc(&p.d_R16, (size_t)p.Q_pad * p.K2 * 2));
+    SVD_CUDA_TRY(cudaMemset(p.d_R16, 0, (size_t)p.Q_pad * p.K2 * 2));
+    SVD_CUDA_TRY(cudaMalloc(&p.d_R32, (size_t)n * p.K2 * 4));
+    SVD_CUDA_TRY(cudaMemset(p.d_R32, 0, (size_t)n * p.K2 * 4));
+    pack_r16_kernel<<<n, 256>>>((const cuDoubleComplex*)G.ptr, (const double*)lam.ptr, n, D, p.Dh, p.K2, p.d_R16,
+                                p.d_R32);
     SVD_CUDA_TRY(cudaGetLastError());
     SVD_CUDA_TRY(cudaDeviceSynchronize());
     return SVDPHAT_OK;
