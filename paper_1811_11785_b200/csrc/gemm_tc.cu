@@ -145,6 +145,9 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, GemmParams p) {
     // MODE 0: producer B + argmax, 1: producer B + store, 2: TMA B + argmax, 3: TMA B + store
     constexpr bool kProducer = (MODE == 0 || MODE == 1);
+    // TMA-B modes have no producer warps: warps 6-9 join the epilogue (frames [128, 256) of the tile), warps 2-5 take
+    // frames [0, 128) (each lane group of TMEM is read by two warps: warp w may access lanes 32 (w % 4) ..)
+    constexpr int kEpiWarps = kProducer ? 4 : 8;
     constexpr int kPairs = Mi * (Mi - 1) / 2;
     constexpr int kUnitsRaw = (BPC == 4) ? kPairs : (kPairs + 1) / 2;
     constexpr int kU = (kUnitsRaw + 7) / 8 * 8;        // units per chunk
@@ -171,7 +174,7 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
         }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&tfull[a], 1);
-            mbar_init(&tempty[a], 4);
+            mbar_init(&tempty[a], kEpiWarps);
         }
         fence_mbar_init();
     }
@@ -240,9 +243,10 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
                 acc_phase ^= 1;
             }
         }
-    } else if (warp < 6) {
+    } else if (warp < 2 + kEpiWarps) {
         // ============================================================ epilogue: TMEM -> registers -> argmax / Z
         const int g = warp & 3;                                    // TMEM lane group this warp may access
+        const int jbeg = (warp < 6) ? 0 : BN / 2, jend = (kEpiWarps == 4 || warp >= 6) ? BN : BN / 2;
         int acc = 0;
         uint32_t acc_phase = 0;
         for (int t = blockIdx.x; t < n_tiles_total; t += gridDim.x) {
@@ -254,11 +258,14 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
             const int row = m * BM + g * 32 + lane;
             const bool row_ok = row < p.rows_valid;
 #pragma unroll 1
-            for (int j0 = 0; j0 < BN; j0 += 32) {
+            for (int j0 = jbeg; j0 < jend; j0 += 32) {
                 uint32_t r[32];
+                const int f0 = n * BN + j0;
+                const bool fok = f0 + lane < p.F;
+                // the frame's running maximum (a possibly stale read is a lower bound: more candidates, never fewer)
+                const unsigned long long prev = (MODE == 2 && fok) ? __ldcg(&p.keys[f0 + lane]) : 0ull;
                 tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + acc * BN + j0, r);
                 tmem_ld_wait();
-                const int f0 = n * BN + j0;
                 if (MODE == 1 || MODE == 3) {
                     if (row_ok) {
 #pragma unroll
@@ -274,22 +281,24 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
                         k[jj] = (row_ok && v == v) ? make_key(v, (uint32_t)row) : 0ull;
                     }
                     const unsigned long long best = transpose_max32(k, lane);
-                    const bool fok = f0 + lane < p.F;
-                    unsigned long long run = 0ull;                 // running maximum of this frame (lane's column)
-                    if (fok && best != 0ull) run = atomicMax(&p.keys[f0 + lane], best);
+                    if (fok && best != 0ull) atomicMax(&p.keys[f0 + lane], best);
                     if (MODE == 2) {
                         // candidates of the exact rescore: rows within SEARCH_TAU of the running FP16 maximum.  The
-                        // exact argmax q* has s16(q*) >= max16 - 2e >= running - SEARCH_TAU, e the FP16 error bound.
-                        run = run > best ? run : best;
-                        const float thr = run ? o2f((uint32_t)(run >> 32)) - SEARCH_TAU : INFINITY;
+                        // exact argmax q* has s16(q*) >= max16 - 2e >= running - SEARCH_TAU (e: FP16 error bound).
+                        const unsigned long long run = prev > best ? prev : best;
+                        const float thr = (fok && run) ? o2f((uint32_t)(run >> 32)) - SEARCH_TAU : INFINITY;
+                        const bool any = best != 0ull && o2f((uint32_t)(best >> 32)) >= thr;
+                        const uint32_t mask = __ballot_sync(0xffffffffu, any);
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj) {
-                            const float t = __shfl_sync(0xffffffffu, thr, jj);
-                            const float v = __uint_as_float(r[jj]);
-                            if (row_ok && v >= t && f0 + jj < p.F) {
-                                const int idx = atomicAdd(&p.ccnt[f0 + jj], 1);
-                                if (idx < SEARCH_CAP)
-                                    p.cand[(int64_t)(f0 + jj) * SEARCH_CAP + idx] = make_key(v, (uint32_t)row);
+                            if (mask & (1u << jj)) {
+                                const float tj = __shfl_sync(0xffffffffu, thr, jj);
+                                const float v = __uint_as_float(r[jj]);
+                                if (row_ok && v >= tj) {
+                                    const int idx = atomicAdd(&p.ccnt[f0 + jj], 1);
+                                    if (idx < SEARCH_CAP)
+                                        p.cand[(int64_t)(f0 + jj) * SEARCH_CAP + idx] = make_key(v, (uint32_t)row);
+                                }
                             }
                         }
                     }

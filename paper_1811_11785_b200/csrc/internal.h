@@ -181,7 +181,7 @@ constexpr int MAX_KSPLIT = 32;               // cap on K splits (chunk ranges) o
 // frame's running FP16 maximum.  SEARCH_TAU = 2.5e-3 >= twice the FP16 error bound of a unit-vector dot product
 // (2^-10 + FP32 accumulation), so the exact argmax is always a candidate; lists longer than SEARCH_CAP fall back to
 // an exact scan of every class for that frame.
-constexpr int SEARCH_CAP = 32;
+constexpr int SEARCH_CAP = 128;
 constexpr float SEARCH_TAU = 2.5e-3f;
 cudaError_t launch_rescore(const Plan& p, int F, cudaStream_t s);
 struct ProjShape {
