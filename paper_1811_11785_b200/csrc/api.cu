@@ -204,7 +204,7 @@ struct svdphat_plan_s {
         if (p.ev_z) cudaEventDestroy(p.ev_z);
         void* bufs[] = {p.d_W16,   p.d_V16,   p.d_R16,   p.d_rep,   p.d_delay,     p.d_window,      p.d_twN,
                         p.d_P16,   p.d_keys,  p.d_Z32,   p.d_Zs16,  p.d_zflag,     p.d_stage,       p.d_doa_stage,
-                        p.d_R32,   p.d_Zn32,  p.d_cand,  p.d_ccnt,
+                        p.d_R32,   p.d_Zn32,  p.d_cand,  p.d_ccnt,  p.d_Smap,
                         p.d_score_stage, p.d_S, p.d_cls, p.d_dirs, p.d_Ypart, p.d_fold_cls};
         for (void* b : bufs)
             if (b) cudaFree(b);
@@ -560,6 +560,12 @@ static svdphat_status plan_create_impl(const svdphat_plan_desc* d, svdphat_plan_
         SVD_CUDA_TRY(cudaMemset(p.d_Zn32, 0, Fp * p.K2 * sizeof(float)));
         SVD_CUDA_TRY(cudaMalloc(&p.d_cand, Fp * SEARCH_CAP * sizeof(unsigned long long)));
         SVD_CUDA_TRY(cudaMalloc(&p.d_ccnt, Fp * sizeof(int)));
+        const int64_t map_bytes = Fp * (int64_t)p.Q_pad * (int64_t)sizeof(float);
+        if (map_bytes <= (64ll << 20)) {        // small batches: score map + per-frame rescore (see internal.h)
+            SVD_CUDA_TRY(cudaMalloc(&p.d_Smap, map_bytes));
+            p.search_map = true;
+            p.bytes_ws += map_bytes;
+        }
         p.bytes_ws += zbytes * p.zsplit_max + Fp * p.K2 * 6 + Fp * 8 + Fp * SEARCH_CAP * 8;
         if (!encode_2d(&p.tm_Zs, p.d_Zs16, Fp, p.K2, 256))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(Zs) failed");
@@ -677,7 +683,8 @@ static svdphat_status localize_impl(Plan& p, const Band& b, int32_t method, cons
                             [&] { return launch_finalize(p, SVDPHAT_METHOD_SRP, F, doas, scores, sr); }));
     }
     if (method & SVDPHAT_METHOD_SVD) {
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_SEARCH, sv, [&] { return launch_gemm(p, b, 2, F, sv); }));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_SEARCH, sv,
+                            [&] { return launch_gemm(p, b, p.search_map ? 5 : 2, F, sv); }));
         SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_RESCORE, sv, [&] { return launch_rescore(p, F, sv); }));
         if (fork)
             SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_FINALIZE, sv,

@@ -379,8 +379,84 @@ cudaError_t launch_zsplit(const Plan& p, const Band& b, int F, cudaStream_t s, b
     return cudaErrorInvalidValue;                 // 2*Zh > 8192 columns: excluded at plan creation
 }
 
+// Small batches: exact rescore from the stored score map (search GEMM mode 5).  CTA per frame: the frame's FP16-input
+// maximum over the classes, then every class within SEARCH_TAU of it is rescored in FP32 (a warp per candidate, lanes
+// over K) and the best (lowest class on ties) becomes the frame's SVD key.
+constexpr int RM_THREADS = 256;
+constexpr int RM_CAND = 512;                          // candidates held in shared memory (more: rescored in passes)
+__global__ void __launch_bounds__(RM_THREADS)
+    rescore_map_kernel(const float* __restrict__ S, int ldS, int Q, const float* __restrict__ R32,
+                       const float* __restrict__ Zn, int K2, int F, unsigned long long* __restrict__ keys) {
+    __shared__ float s_red[RM_THREADS / 32];
+    __shared__ unsigned long long s_best[RM_THREADS / 32];
+    __shared__ int s_cand[RM_CAND];
+    __shared__ int s_n;
+    const int f = blockIdx.x;
+    if (f >= F) return;
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const float* row = S + (int64_t)f * ldS;
+    float m = -INFINITY;
+    for (int q = t; q < Q; q += RM_THREADS) m = fmaxf(m, row[q]);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) s_red[warp] = m;
+    __syncthreads();
+    m = s_red[0];
+#pragma unroll
+    for (int w = 1; w < RM_THREADS / 32; ++w) m = fmaxf(m, s_red[w]);
+    const float thr = m - SEARCH_TAU;
+    const float4* zf = reinterpret_cast<const float4*>(Zn + (int64_t)f * K2);
+    const int n4 = K2 >> 2;
+    unsigned long long best = 0ull;
+    for (int q0 = 0; q0 < Q; q0 += RM_CAND * 8) {            // candidate gathering in passes of <= RM_CAND
+        if (t == 0) s_n = 0;
+        __syncthreads();
+        const int q1 = min(Q, q0 + RM_CAND * 8);
+        for (int q = q0 + t; q < q1; q += RM_THREADS)
+            if (row[q] >= thr) {
+                const int i = atomicAdd(&s_n, 1);
+                if (i < RM_CAND) s_cand[i] = q;
+            }
+        __syncthreads();
+        const int n = min(s_n, RM_CAND);
+        const bool overflow = s_n > RM_CAND;
+        // overflow (a flat map): every class of this pass is rescored
+        const int cnt = overflow ? q1 - q0 : n;
+        for (int c = warp; c < cnt; c += RM_THREADS / 32) {
+            const int q = overflow ? q0 + c : s_cand[c];
+            const float4* r = reinterpret_cast<const float4*>(R32 + (int64_t)q * K2);
+            float acc = 0.f;
+            for (int i = lane; i < n4; i += 32) {
+                const float4 a = __ldg(r + i), b = zf[i];
+                acc = fmaf(a.x, b.x, acc);
+                acc = fmaf(a.y, b.y, acc);
+                acc = fmaf(a.z, b.z, acc);
+                acc = fmaf(a.w, b.w, acc);
+            }
+#pragma unroll
+            for (int o = 16; o >= 1; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+            const unsigned long long kq =
+                acc == acc ? ((unsigned long long)f2o_dev(acc) << 32) | (0xFFFFFFFFull - q) : 0ull;
+            best = kq > best ? kq : best;
+        }
+        __syncthreads();
+    }
+    if (lane == 0) s_best[warp] = best;
+    __syncthreads();
+    if (t == 0) {
+        unsigned long long b = s_best[0];
+        for (int w = 1; w < RM_THREADS / 32; ++w) b = s_best[w] > b ? s_best[w] : b;
+        keys[f] = m > -INFINITY ? b : 0ull;
+    }
+}
+
 cudaError_t launch_rescore(const Plan& p, int F, cudaStream_t s) {
     if (F <= 0) return cudaSuccess;
+    if (p.search_map) {
+        rescore_map_kernel<<<F, RM_THREADS, 0, s>>>(p.d_Smap, p.Q_pad, p.Q_eff, p.d_R32, p.d_Zn32, p.K2, F,
+                                                    p.d_keys + p.F_pad);
+        return cudaGetLastError();
+    }
     rescore_kernel<<<(F * 32 + 255) / 256, 256, 0, s>>>(p.d_keys + 2 * p.F_pad, p.d_cand, p.d_ccnt, p.d_R32,
                                                         p.d_Zn32, p.K2, p.Q_eff, F, p.d_keys + p.F_pad);
     return cudaGetLastError();

@@ -973,7 +973,7 @@ constexpr int P_MAX_STAGES = 8;
 
 // Producer warps of gemm2p_kernel: this thread's A row (PART 0: Re x, PART 1: Im x of frame f, eqs. 3, 7) for the bin
 // chunks [w.c0, w.c1), one 16-unit slab per stage (the last slab of a chunk holds kU % 16 units when that is 8).
-template <int Mi, int BPC, int PART>
+template <int Mi, int BPC, int PART, int STG>
 __device__ __forceinline__ void produce_x_part(const GemmParams& p, const Unit& w, int f, bool valid, uint8_t* smem,
                                                uint64_t* full, uint64_t* empty, int& stage, uint32_t& phase,
                                                uint32_t row_off, uint32_t xr) {
@@ -1066,7 +1066,7 @@ __device__ __forceinline__ void produce_x_part(const GemmParams& p, const Unit& 
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive_cluster(&full[stage], 0);   // the leader's barrier
-                if (++stage == p.stages) {
+                if (++stage == STG) {
                     stage = 0;
                     phase ^= 1;
                 }
@@ -1075,16 +1075,20 @@ __device__ __forceinline__ void produce_x_part(const GemmParams& p, const Unit& 
     }
 }
 
-template <int Mi, int BPC>
+// NMMA: MMAs per K step (tile rows nt = NMMA * nmma); STG: ring stages (6 for nt <= 320, 4 up to 512).  The MMA issue
+// loop is unrolled over the SP slabs of a bin chunk with compile-time stage/half-slab logic (ncu r02: a runtime n_mma
+// loop, half-slab test and stage multiply cost ~185 issue instructions per slab and left the tensor pipe 45% active).
+template <int Mi, int BPC, int NMMA, int STG>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     gemm2p_kernel(const __grid_constant__ CUtensorMap tmV, GemmParams p) {
     constexpr int kUnitsRaw = (BPC == 4) ? Mi * (Mi - 1) / 2 : (Mi * (Mi - 1) / 2 + 1) / 2;
     constexpr int kU = (kUnitsRaw + 7) / 8 * 8;
+    constexpr int kSP = (kU + 15) / 16;                     // slabs per bin chunk
     constexpr bool kHalf = (kU % 16 == 8);                  // the last slab of a chunk holds 8 units: K = 32
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     // stage s: [A: 128 rows x 128 B][B: nt/2 V rows x 128 B, as n_mma blocks of nmma/2 rows]
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.stages * p.stage_bytes);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + STG * p.stage_bytes);
     uint64_t* empty = full + P_MAX_STAGES;
     uint64_t* tfull = empty + P_MAX_STAGES;
     uint64_t* tempty = tfull + 1;
@@ -1100,7 +1104,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     const uint32_t idesc = umma_idesc_f16(256, (uint32_t)p.nmma);
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < p.stages; ++s) {
+        for (int s = 0; s < STG; ++s) {
             mbar_init(&full[s], 1 + 2 * NPW2);              // leader's TMA (expect_tx) + producers of both CTAs
             mbar_init(&empty[s], 1);
         }
@@ -1127,10 +1131,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
                     mbar_wait(&empty[stage], phase ^ 1);
                     if (leader) mbar_arrive_expect_tx(&full[stage], bytes);
                     uint8_t* sB = smem + stage * p.stage_bytes + P_A_BYTES;
-                    for (int j = 0; j < p.n_mma; ++j)
+#pragma unroll
+                    for (int j = 0; j < NMMA; ++j)
                         tma_load_2d_2sm(sB + j * hm * (BK * 2), &tmV, ks * BK, w.n * nt + j * p.nmma + (int)rank * hm,
                                         &full[stage]);
-                    if (++stage == p.stages) {
+                    if (++stage == STG) {
                         stage = 0;
                         phase ^= 1;
                     }
@@ -1139,38 +1144,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
         }
     } else if (warp == 1) {
         if (leader) {                                       // converged-warp MMA issue (see gemm2_kernel)
-            const uint64_t desc0 = umma_desc_sw128(smem_u32(smem));
-            const uint64_t sdesc = (uint64_t)(p.stage_bytes >> 4), bdesc = (uint64_t)(P_A_BYTES >> 4);
-            const uint64_t jdesc = (uint64_t)((hm * BK * 2) >> 4);
+            const uint32_t lo0 = umma_desc_lo(smem_u32(smem)), hi = umma_desc_hi_sw128();
+            const uint32_t sdesc = (uint32_t)(p.stage_bytes >> 4);
+            const uint32_t bdesc = (uint32_t)(P_A_BYTES >> 4), jdesc = (uint32_t)((hm * BK * 2) >> 4);
             int stage = 0;
             uint32_t phase = 0, acc_phase = 0;
+            uint32_t alo = lo0;                             // A descriptor low word of the current stage
             for (int t = pair; t < units; t += n_pairs) {
                 const Unit w = unit_of_f(p, t);
                 mbar_wait(tempty, acc_phase ^ 1);
                 tc_fence_after();
-                int lp = 0;                                 // slab within the bin chunk
-                for (int ks = w.k0; ks < w.k1; ++ks) {
-                    mbar_wait(&full[stage], phase);
-                    tc_fence_after();
-                    const uint64_t ad = desc0 + (uint64_t)stage * sdesc;
-                    const bool half = kHalf && lp == p.spc - 1;
-                    const uint32_t acc0 = ks != w.k0;
-                    for (int j = 0; j < p.n_mma; ++j) {
-                        const uint32_t d_tmem = tmem_base + (uint32_t)(j * p.nmma);
-                        const uint64_t bd = ad + bdesc + (uint64_t)j * jdesc;
-                        umma_f16_2sm_warp(d_tmem, ad, bd, idesc, acc0);
-                        umma_f16_2sm_warp(d_tmem, ad + 2, bd + 2, idesc, 1u);
-                        if (!half) {
-                            umma_f16_2sm_warp(d_tmem, ad + 4, bd + 4, idesc, 1u);
-                            umma_f16_2sm_warp(d_tmem, ad + 6, bd + 6, idesc, 1u);
+                uint32_t acc0 = 0u;
+                for (int c = w.c0; c < w.c1; ++c) {
+#pragma unroll
+                    for (int sl = 0; sl < kSP; ++sl) {
+                        mbar_wait(&full[stage], phase);
+                        tc_fence_after();
+#pragma unroll
+                        for (int j = 0; j < NMMA; ++j) {
+                            const uint32_t d_tmem = tmem_base + (uint32_t)(j * p.nmma);
+                            if (kHalf && sl == kSP - 1)   // compile-time after unrolling: 8 units = K 32
+                                umma_f16_2sm_steps<2>(d_tmem, alo, alo + bdesc + j * jdesc, hi, idesc, acc0);
+                            else
+                                umma_f16_2sm_steps<4>(d_tmem, alo, alo + bdesc + j * jdesc, hi, idesc, acc0);
+                        }
+                        acc0 = 1u;
+                        umma_commit_2sm_warp(&empty[stage], 0x3);
+                        if (++stage == STG) {
+                            stage = 0;
+                            phase ^= 1;
+                            alo = lo0;
+                        } else {
+                            alo += sdesc;
                         }
                     }
-                    umma_commit_2sm_warp(&empty[stage], 0x3);
-                    if (++stage == p.stages) {
-                        stage = 0;
-                        phase ^= 1;
-                    }
-                    if (++lp == p.spc) lp = 0;
                 }
                 umma_commit_2sm_warp(tfull, 0x3);
                 acc_phase ^= 1;
@@ -1215,9 +1222,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
             const Unit w = unit_of_f(p, t);
             const int f = w.m * 128 + (int)rank * 64 + (tp & 63);
             if (tp < 64)
-                produce_x_part<Mi, BPC, 0>(p, w, f, f < p.F, smem, full, empty, stage, phase, row_off, xr);
+                produce_x_part<Mi, BPC, 0, STG>(p, w, f, f < p.F, smem, full, empty, stage, phase, row_off, xr);
             else
-                produce_x_part<Mi, BPC, 1>(p, w, f, f < p.F, smem, full, empty, stage, phase, row_off, xr);
+                produce_x_part<Mi, BPC, 1, STG>(p, w, f, f < p.F, smem, full, empty, stage, phase, row_off, xr);
         }
     }
 
@@ -1247,7 +1254,9 @@ static cudaError_t set_attr_pair() {
     if ((e = cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, 0, true>, attr, sm))) return e;
     if ((e = cudaFuncSetAttribute(gemm2_kernel<Mi, BPC, 1, true>, attr, sm))) return e;
     if ((e = cudaFuncSetAttribute(gemm2f_kernel<Mi, BPC>, attr, sm))) return e;
-    return cudaFuncSetAttribute(gemm2p_kernel<Mi, BPC>, attr, 227 * 1024);
+    if ((e = cudaFuncSetAttribute(gemm2p_kernel<Mi, BPC, 1, 6>, attr, 227 * 1024))) return e;
+    if ((e = cudaFuncSetAttribute(gemm2p_kernel<Mi, BPC, 2, 6>, attr, 227 * 1024))) return e;
+    return cudaFuncSetAttribute(gemm2p_kernel<Mi, BPC, 2, 4>, attr, 227 * 1024);
 }
 
 cudaError_t gemm_set_attributes() {
@@ -1375,7 +1384,7 @@ cudaError_t launch_gemm(const Plan& p, const Band& b, int mode, int F, cudaStrea
         gp.n_slabs = (int)(p.L.K_total / BK);
         gp.rows_valid = 2 * p.Dh;
         gp.m_tiles = (2 * p.Dh) / BM;
-    } else {                           // 2: SVD search + argmax; 4: its power map Re{Dhat Zhat}[f][class] -> S
+    } else {                           // 2: SVD search + argmax; 4/5: its score map Re{Dhat Zhat}[f][class] -> S / Smap
         A = &p.tm_R;
         B = &p.tm_Zs;
         gp.n_slabs = p.K2 / BK;
@@ -1386,7 +1395,7 @@ cudaError_t launch_gemm(const Plan& p, const Band& b, int mode, int F, cudaStrea
             gp.cand = p.d_cand;
             gp.ccnt = p.d_ccnt;
         } else {
-            gp.Z = p.d_S;
+            gp.Z = mode == 5 ? p.d_Smap : p.d_S;
             gp.ldz = p.Q_pad;
         }
     }
@@ -1414,15 +1423,19 @@ cudaError_t launch_gemm(const Plan& p, const Band& b, int mode, int F, cudaStrea
             gp.ldz = 2 * p.Zh;
             gp.zh = p.Zh;
             gp.stage_bytes = P_A_BYTES + (p.proj_nt / 2) * BK * 2;
-            gp.stages = (227 * 1024 - 1024 - 256) / gp.stage_bytes;
-            gp.stages = gp.stages > P_MAX_STAGES ? P_MAX_STAGES : gp.stages;
+            gp.stages = 1024 + 6 * gp.stage_bytes + 256 <= 227 * 1024 ? 6 : 4;
             const int units = gp.m_tiles * gp.n_tiles * gp.ksplit;
             if (units == 0) return cudaSuccess;
             const int pairs = units < npairs ? units : npairs;
             const size_t smem = 1024 + (size_t)gp.stages * gp.stage_bytes + 256;
 #define SVD_PROJP(MI, BP)                                                                                        \
     if (p.L.Mi == MI) {                                                                                         \
-        gemm2p_kernel<MI, BP><<<2 * pairs, THREADS2, smem, s>>>(*A, gp);                                        \
+        if (gp.n_mma == 1)                                                                                      \
+            gemm2p_kernel<MI, BP, 1, 6><<<2 * pairs, THREADS2, smem, s>>>(*A, gp);                              \
+        else if (gp.stages == 6)                                                                                \
+            gemm2p_kernel<MI, BP, 2, 6><<<2 * pairs, THREADS2, smem, s>>>(*A, gp);                              \
+        else                                                                                                    \
+            gemm2p_kernel<MI, BP, 2, 4><<<2 * pairs, THREADS2, smem, s>>>(*A, gp);                              \
         return cudaGetLastError();                                                                              \
     }
             SVD_PROJP(4, 4)
@@ -1456,7 +1469,7 @@ cudaError_t launch_gemm(const Plan& p, const Band& b, int mode, int F, cudaStrea
     const int grid = tiles < p.num_sms ? tiles : p.num_sms;
     if (tiles == 0) return cudaSuccess;
     if (mode == 2) return launch_one<4, 4, 2>(*A, *B, gp, grid, s);
-    if (mode == 4) return launch_one<4, 4, 3>(*A, *B, gp, grid, s);
+    if (mode == 4 || mode == 5) return launch_one<4, 4, 3>(*A, *B, gp, grid, s);
     if (mode == 0 && srp_split_ways(p, b, F) > 1) {
         // small batch: fewer units than half the CTA pairs -> split K into chunk ranges with partial power maps
         const int S = srp_split_ways(p, b, F);

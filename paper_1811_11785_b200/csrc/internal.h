@@ -87,6 +87,10 @@ struct Plan {
     float* d_Zn32 = nullptr;      // [F_pad][K2] FP32 Zhat = Z/||Z|| [Re | Im] (rescore)
     unsigned long long* d_cand = nullptr;  // [F_pad][SEARCH_CAP] search candidates (FP16 score, class)
     int* d_ccnt = nullptr;        // [F_pad] candidates per frame
+    // small batches (F_pad x Q_pad FP32 <= 64 MB): the search GEMM stores its FP16-input score map and the rescore
+    // scans it per frame (all row tiles of a frame run concurrently there, so running-maximum lists would overflow)
+    float* d_Smap = nullptr;      // [F_pad][Q_pad]
+    bool search_map = false;
     int V_rows = 0;               // rows of V16: proj_ntiles * proj_nt (pair projection) or 2*Dh (1-CTA)
     int proj_nt = 0;              // V rows per pair tile of the frames-on-M projection (multiple of 32, <= 256)
     int proj_ntiles = 0;          // V row tiles
@@ -170,7 +174,8 @@ void set_error(const std::string& msg);
 cudaError_t launch_stft_phat(const Plan& p, const Band& b, const float* audio, int64_t cs, int64_t fstride, int F,
                              cudaStream_t s);
 // mode: 0 = SRP argmax (A = W16, B = producer), 1 = SVD GEMM1 store Z (A = V16, B = producer),
-//       2 = SVD search argmax (A = R16, B = Zs16 via TMA), 3 = SRP power map -> d_S, 4 = SVD search power map -> d_S
+//       2 = SVD search argmax + candidate lists (A = R16, B = Zs16 via TMA), 3 = SRP power map -> d_S,
+//       4 = SVD search power map -> d_S, 5 = SVD search score map -> d_Smap (small batches, rescored per frame)
 // both: a localize(BOTH) call, where the SRP tail rows travel through the projection (Plan::tail_n)
 cudaError_t launch_gemm(const Plan& p, const Band& b, int mode, int F, cudaStream_t s, bool both = false);
 cudaError_t launch_zsplit(const Plan& p, const Band& b, int F, cudaStream_t s, bool both = false);

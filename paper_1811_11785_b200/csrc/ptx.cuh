@@ -201,6 +201,48 @@ __device__ __forceinline__ void umma_commit_2sm_warp(uint64_t* bar, uint16_t mas
         ::"r"(smem_u32(bar)), "h"(mask)
         : "memory");
 }
+// Descriptor words of umma_desc_sw128: lo = (smem address >> 4) | LBO field, hi = SBO | version | layout.  Smem
+// addresses stay below 256 KB, so advancing the start address never carries out of the low word.
+__device__ __forceinline__ uint32_t umma_desc_lo(uint32_t smem_addr) {
+    return ((smem_addr >> 4) & 0x3FFFu) | ((16u >> 4) << 16);
+}
+__host__ __device__ constexpr uint32_t umma_desc_hi_sw128() { return (1024u >> 4) | (1u << 14) | (2u << 29); }
+
+// NK consecutive K = 16 steps of a CTA-pair MMA (one 32-byte K step = +2 in both descriptors' low words) in ONE asm
+// block with one elect.sync: ptxas then moves the two base words into uniform registers once and advances them in the
+// uniform datapath, instead of an ELECT / R2UR.BROADCAST / VOTEU sequence per MMA (ncu r02: ~23 issue instructions per
+// MMA, a dependent chain that starved the tensor pipe at N = 160).  accumulate applies to the first step only.
+template <int NK>
+__device__ __forceinline__ void umma_f16_2sm_steps(uint32_t tmem_d, uint32_t a_lo, uint32_t b_lo, uint32_t hi,
+                                                   uint32_t idesc, uint32_t accumulate) {
+    static_assert(NK == 2 || NK == 4, "2 or 4 K steps");
+    if constexpr (NK == 4) {
+        asm volatile(
+            "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a0, b0, a1, b1, a2, b2, a3, b3;\n\t.reg .b32 x, y;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+            "mov.b64 a0, {%1, %3};\n\tmov.b64 b0, {%2, %3};\n\t"
+            "add.u32 x, %1, 2;\n\tadd.u32 y, %2, 2;\n\tmov.b64 a1, {x, %3};\n\tmov.b64 b1, {y, %3};\n\t"
+            "add.u32 x, %1, 4;\n\tadd.u32 y, %2, 4;\n\tmov.b64 a2, {x, %3};\n\tmov.b64 b2, {y, %3};\n\t"
+            "add.u32 x, %1, 6;\n\tadd.u32 y, %2, 6;\n\tmov.b64 a3, {x, %3};\n\tmov.b64 b3, {y, %3};\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a0, b0, %4, p;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %4, t;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a2, b2, %4, t;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a3, b3, %4, t;\n\t}" ::"r"(tmem_d),
+            "r"(a_lo), "r"(b_lo), "r"(hi), "r"(idesc), "r"(accumulate)
+            : "memory");
+    } else {
+        asm volatile(
+            "{\n\t.reg .pred e, p, t;\n\t.reg .b64 a0, b0, a1, b1;\n\t.reg .b32 x, y;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %5, 0;\n\tsetp.eq.b32 t, 1, 1;\n\t"
+            "mov.b64 a0, {%1, %3};\n\tmov.b64 b0, {%2, %3};\n\t"
+            "add.u32 x, %1, 2;\n\tadd.u32 y, %2, 2;\n\tmov.b64 a1, {x, %3};\n\tmov.b64 b1, {y, %3};\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a0, b0, %4, p;\n\t"
+            "@e tcgen05.mma.cta_group::2.kind::f16 [%0], a1, b1, %4, t;\n\t}" ::"r"(tmem_d),
+            "r"(a_lo), "r"(b_lo), "r"(hi), "r"(idesc), "r"(accumulate)
+            : "memory");
+    }
+}
+
 // A operand from TMEM ("TS" form): [a_tmem] is the TMEM address of this CTA's 128 rows x 16 K (8 columns).
 __device__ __forceinline__ void umma_f16_2sm_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t bdesc, uint32_t idesc,
                                                 uint32_t accumulate) {
