@@ -64,12 +64,18 @@ typedef struct {
  *   NO_SRP_FOLD   SRP GEMM on one row per steering class instead of antipodal fold rows (R22);
  *   NO_SVD_FOLD   complex V_D (2D real-split rows) instead of the real-basis V_D of a centrally symmetric grid;
  *   ONE_CTA_SRP   1-CTA 128-row SRP GEMM tiles instead of CTA pairs (implies NO_SRP_FOLD);
- *   ONE_CTA_PROJ  1-CTA V-on-M projection GEMM instead of the frames-on-M CTA-pair kernel (implies NO_SVD_FOLD). */
+ *   ONE_CTA_PROJ  1-CTA V-on-M projection GEMM instead of the frames-on-M CTA-pair kernel (implies NO_SVD_FOLD);
+ *   NO_DAS        SRP-PHAT always through eq. 9's GEMM Y = Re{W X}, never through the delay-and-sum form of eq. 5
+ *                 (Y_q = 1/2 sum_k |sum_m e_m[k] e^{j 2 pi k delta_qm / N}|^2 - n_k, tau_qij = delta_qi - delta_qj), which
+ *                 the library uses by default for M >= 12 on batches that fill the GPU (NEXT-4);
+ *   DAS           the delay-and-sum form for every M and every batch size. */
 enum {
     SVDPHAT_OPT_NO_SRP_FOLD = 1,
     SVDPHAT_OPT_NO_SVD_FOLD = 2,
     SVDPHAT_OPT_ONE_CTA_SRP = 4,
-    SVDPHAT_OPT_ONE_CTA_PROJ = 8
+    SVDPHAT_OPT_ONE_CTA_PROJ = 8,
+    SVDPHAT_OPT_NO_DAS = 16,
+    SVDPHAT_OPT_DAS = 32
 };
 
 typedef struct {
@@ -195,7 +201,9 @@ enum {
     SVDPHAT_STAGE_SVD_NORM = 4,    /* Zhat = Z / ||Z|| (FP16 search operand, FP32 rescore operand)              */
     SVDPHAT_STAGE_SVD_SEARCH = 5,  /* Re{Dhat_q Zhat} in FP16 + fused running argmax and candidate lists (eq. 14)  */
     SVDPHAT_STAGE_FINALIZE = 6,    /* Y_q of the chosen q (eq. 5; Alg. 1 online step 4)                         */
-    SVDPHAT_STAGE_SVD_RESCORE = 7  /* exact FP32 Re{Dhat_q Zhat} of the search candidates -> q_bar (eqs. 14-15)  */
+    SVDPHAT_STAGE_SVD_RESCORE = 7, /* exact FP32 Re{Dhat_q Zhat} of the search candidates -> q_bar (eqs. 14-15)  */
+    SVDPHAT_STAGE_SRP_BINS = 8,    /* phasors re-laid per bin for the delay-and-sum SRP GEMM                     */
+    SVDPHAT_STAGE_SRP_DAS = 9      /* delay-and-sum SRP: per-bin GEMM, sum of |a_q[k]|^2 over bins, argmax (eq. 5) */
 };
 svdphat_status svdphat_profile_begin(svdphat_plan_t plan, int32_t capacity);
 int32_t svdphat_profile_end(svdphat_plan_t plan, int32_t* stage_ids, float* ms, int32_t max);

@@ -16,11 +16,11 @@ OK, INVALID_ARG, ALLOC, CUDA, NUMERIC, UNSUPPORTED, TOO_LARGE = range(7)
 FIELD_FAR, FIELD_NEAR = 0, 1
 METHOD_SRP, METHOD_SVD, METHOD_BOTH = 1, 2, 3
 STAGES = {1: "stft_phat", 2: "srp_gemm", 3: "svd_proj", 4: "svd_norm", 5: "svd_search", 6: "finalize",
-          7: "svd_rescore"}
+          7: "svd_rescore", 8: "srp_bins", 9: "srp_das"}
 _METHOD = {"srp": METHOD_SRP, "svd": METHOD_SVD, "both": METHOD_BOTH}
 DUMP_PHASORS, DUMP_Z, DUMP_CLASS_REP, DUMP_KEYS, DUMP_POWER = 1, 2, 3, 4, 5
 # svdphat_plan_desc.options: equivalent alternative kernels (tests / A-B measurements), 0 = product configuration
-OPT_NO_SRP_FOLD, OPT_NO_SVD_FOLD, OPT_ONE_CTA_SRP, OPT_ONE_CTA_PROJ = 1, 2, 4, 8
+OPT_NO_SRP_FOLD, OPT_NO_SVD_FOLD, OPT_ONE_CTA_SRP, OPT_ONE_CTA_PROJ, OPT_NO_DAS, OPT_DAS = 1, 2, 4, 8, 16, 32
 
 
 class PlanDesc(C.Structure):

@@ -20,7 +20,7 @@ NVCC = os.path.join(CUDA, "bin", "nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xptxas", "-v", "--expt-relaxed-constexpr",
          "-I" + os.path.join(ROOT, "include")]
-SOURCES = ["api.cu", "setup.cu", "stft_phat.cu", "gemm_tc.cu", "finalize.cu"]
+SOURCES = ["api.cu", "setup.cu", "stft_phat.cu", "gemm_tc.cu", "finalize.cu", "das.cu"]
 HEADERS = ["internal.h", "ptx.cuh"]
 
 

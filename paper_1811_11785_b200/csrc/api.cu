@@ -110,6 +110,26 @@ static bool encode_2d(CUtensorMap* tm, const void* base, int64_t rows, int64_t c
     return r == CUDA_SUCCESS;
 }
 
+// 2-D FP16 row-major [rows][cols] tensor, box = cols x box_rows with cols * 2 bytes in {32, 64, 128} and the
+// matching swizzle (the K-major operand rows of das_kernel: one bin's 2 ME halves per row)
+static bool encode_2d_rows(CUtensorMap* tm, const void* base, int64_t rows, int cols, int box_rows) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return false;
+    const CUtensorMapSwizzle sw = cols == 64   ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : cols == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : cols == 16 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                               : CU_TENSOR_MAP_SWIZZLE_NONE;
+    if (sw == CU_TENSOR_MAP_SWIZZLE_NONE) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)cols * 2};
+    cuuint32_t box[2] = {(cuuint32_t)cols, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS;
+}
+
 static Layout make_layout(int M, int N) {
     Layout L;
     L.M = M;
@@ -146,7 +166,7 @@ static svdphat_status validate(const svdphat_plan_desc* d) {
     if (d->rank_D < 0) return fail(SVDPHAT_INVALID_ARG, "rank_D must be >= 0");
     if (d->max_frames < 0 || d->max_frames > (1ll << 26)) return fail(SVDPHAT_INVALID_ARG, "max_frames out of range");
     if (d->options & ~(SVDPHAT_OPT_NO_SRP_FOLD | SVDPHAT_OPT_NO_SVD_FOLD | SVDPHAT_OPT_ONE_CTA_SRP |
-                       SVDPHAT_OPT_ONE_CTA_PROJ))
+                       SVDPHAT_OPT_ONE_CTA_PROJ | SVDPHAT_OPT_NO_DAS | SVDPHAT_OPT_DAS))
         return fail(SVDPHAT_INVALID_ARG, "unknown option bits");
     for (int i = 0; i < 3 * d->M; ++i)
         if (!std::isfinite(d->mic_xyz[i])) return fail(SVDPHAT_INVALID_ARG, "non-finite microphone coordinate");
@@ -205,7 +225,7 @@ struct svdphat_plan_s {
         void* bufs[] = {p.d_W16,   p.d_V16,   p.d_R16,   p.d_rep,   p.d_delay,     p.d_window,      p.d_twN,
                         p.d_P16,   p.d_keys,  p.d_Z32,   p.d_Zs16,  p.d_zflag,     p.d_stage,       p.d_doa_stage,
                         p.d_R32,   p.d_Zn32,  p.d_cand,  p.d_ccnt,  p.d_Smap,
-                        p.d_score_stage, p.d_S, p.d_cls, p.d_dirs, p.d_Ypart, p.d_fold_cls};
+                        p.d_score_stage, p.d_S, p.d_cls, p.d_dirs, p.d_Ypart, p.d_fold_cls, p.d_A16, p.d_E16};
         for (void* b : bufs)
             if (b) cudaFree(b);
     }
@@ -519,6 +539,17 @@ static svdphat_status plan_create_impl(const svdphat_plan_desc* d, svdphat_plan_
         if (st != SVDPHAT_OK) return st;
         if (!encode_2d(&p.tm_W, p.d_W16, p.W_rows, p.K_W, 128))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(W) failed");
+        // delay-and-sum SRP (das.cu) for M >= 12, where its (M-1)/4-fold saving in MMA work beats eq. 9's GEMM
+        const bool use_das = (p.options & SVDPHAT_OPT_DAS) || (!(p.options & SVDPHAT_OPT_NO_DAS) && p.M >= 12);
+        if (use_das) {
+            std::vector<double> dcls((size_t)p.Q_eff * M);
+            for (int c = 0; c < p.Q_eff; ++c)
+                std::memcpy(&dcls[(size_t)c * M], &delay[(size_t)p.rep_q[c] * M], (size_t)M * 8);
+            st = setup_das_operand(p, dcls.data());
+            if (st != SVDPHAT_OK) return st;
+            if (!encode_2d_rows(&p.tm_A, p.d_A16, (int64_t)p.Kb * p.das_rows, 2 * p.das_me, 128))
+                return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(A16) failed");
+        }
     }
     if (p.methods & SVDPHAT_METHOD_SVD) {
         st = setup_svd_operands(p, d_tau, d->rank_D);
@@ -546,6 +577,14 @@ static svdphat_status plan_create_impl(const svdphat_plan_desc* d, svdphat_plan_
     SVD_CUDA_TRY(cudaMemset(p.d_P16, 0, bytes_P16));
     SVD_CUDA_TRY(cudaMalloc(&p.d_keys, 3 * Fp * sizeof(unsigned long long)));
     p.bytes_ws = bytes_P16 + 3 * Fp * 8;
+    if (p.d_A16) {
+        const int64_t bytes_E16 = (int64_t)p.Kb * Fp * 2 * p.das_me * 2;
+        SVD_CUDA_TRY(cudaMalloc(&p.d_E16, bytes_E16));
+        SVD_CUDA_TRY(cudaMemset(p.d_E16, 0, bytes_E16));
+        if (!encode_2d_rows(&p.tm_E, p.d_E16, (int64_t)p.Kb * Fp, 2 * p.das_me, 128))
+            return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(E16) failed");
+        p.bytes_ws += bytes_E16;
+    }
     if (p.methods & SVDPHAT_METHOD_SVD) {
         // split-K partial buffers: as many splits (<= MAX_KSPLIT) as fit in ~256 MB
         const int64_t zbytes = Fp * 2 * p.Zh * (int64_t)sizeof(float);
@@ -585,6 +624,7 @@ static svdphat_status plan_create_impl(const svdphat_plan_desc* d, svdphat_plan_
         }
     }
     SVD_CUDA_TRY(gemm_set_attributes());
+    SVD_CUDA_TRY(das_set_attributes());
     SVD_CUDA_TRY(stft_set_attributes());
     SVD_CUDA_TRY(topk_set_attributes());
     if ((p.methods & SVDPHAT_METHOD_BOTH) == SVDPHAT_METHOD_BOTH) {
@@ -664,10 +704,16 @@ static svdphat_status localize_impl(Plan& p, const Band& b, int32_t method, cons
     }
     int32_t* const doas[2] = {doa_srp, doa_svd};
     float* const scores[2] = {sc_srp, sc_svd};
+    // SRP: the delay-and-sum GEMM (das.cu) when the plan has it and the batch fills the CTA pairs, else eq. 9's GEMM
+    const bool das = (method & SVDPHAT_METHOD_SRP) && das_active(p, F);
     // SRP tail rows scored through the projection: BOTH calls on the argmax GEMM path (not the small-batch split)
-    const bool both = method == SVDPHAT_METHOD_BOTH && p.tail_n > 0 && srp_split_ways(p, b, F) == 1;
-    if (method & SVDPHAT_METHOD_SRP)
+    const bool both = method == SVDPHAT_METHOD_BOTH && !das && p.tail_n > 0 && srp_split_ways(p, b, F) == 1;
+    if (das) {
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_BINS, sr, [&] { return launch_das_bins(p, b, F, sr); }));
+        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_DAS, sr, [&] { return launch_das(p, b, F, sr); }));
+    } else if (method & SVDPHAT_METHOD_SRP) {
         SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_GEMM, sr, [&] { return launch_gemm(p, b, 0, F, sr, both); }));
+    }
     if (method & SVDPHAT_METHOD_SVD) {
         SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_PROJ, sv, [&] { return launch_gemm(p, b, 1, F, sv); }));
         SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_NORM, sv, [&] { return launch_zsplit(p, b, F, sv, both); }));

@@ -124,21 +124,6 @@ __device__ __forceinline__ uint32_t h2fma(uint32_t a, uint32_t b, uint32_t c) {
     return *reinterpret_cast<uint32_t*>(&r);
 }
 
-// u64 max-reduce of 32 columns across the 32 lanes of a warp; afterwards lane l holds column l's maximum.
-__device__ __forceinline__ unsigned long long transpose_max32(unsigned long long (&k)[32], int lane) {
-#pragma unroll
-    for (int h = 16; h >= 1; h >>= 1) {
-        const bool upper = (lane & h) != 0;
-#pragma unroll
-        for (int c = 0; c < h; ++c) {
-            unsigned long long send = upper ? k[c] : k[c + h];
-            unsigned long long mine = upper ? k[c + h] : k[c];
-            unsigned long long recv = __shfl_xor_sync(0xffffffffu, send, h);
-            k[c] = mine > recv ? mine : recv;
-        }
-    }
-    return k[0];
-}
 
 template <int Mi, int BPC, int MODE>
 __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)

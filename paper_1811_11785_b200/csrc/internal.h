@@ -106,12 +106,20 @@ struct Plan {
     float* d_S = nullptr;
     int* d_cls = nullptr;
     float4* d_dirs = nullptr;     // [Q_eff] unit direction of each class representative (from the array centroid)
-    int64_t bytes_W = 0, bytes_V = 0, bytes_R = 0, bytes_ws = 0;
+    // delay-and-sum SRP (das.cu, NEXT-4): per-bin steering rows A16[Kb][das_rows][2 das_me] (Re / Im rows of each
+    // class) and the frames' phasors re-laid per bin, E16[Kb][F_pad][2 das_me]
+    int das_me = 0;               // microphones per K block (8, 16, 32): K = 2 das_me per bin
+    int das_rows = 0;             // 2 Q_eff rounded up to 256
+    __half* d_A16 = nullptr;
+    __half* d_E16 = nullptr;
+    int64_t bytes_W = 0, bytes_V = 0, bytes_R = 0, bytes_ws = 0, bytes_A = 0;
     // TMA descriptors
     alignas(64) CUtensorMap tm_W;
     alignas(64) CUtensorMap tm_V;
     alignas(64) CUtensorMap tm_R;
     alignas(64) CUtensorMap tm_Zs;
+    alignas(64) CUtensorMap tm_A;     // A16 as [Kb * das_rows][2 das_me], box 2 das_me x 128
+    alignas(64) CUtensorMap tm_E;     // E16 as [Kb * F_pad][2 das_me], box 2 das_me x 128
     int num_sms = 148;
     bool pair_srp = true;          // SRP GEMM on CTA pairs (cta_group::2); Q_pad is then a multiple of 256
     // host-buffer path: two staging slots + a copy stream so chunk i+1's H2D overlaps chunk i's compute
@@ -204,7 +212,15 @@ cudaError_t gemm_set_attributes();   // per-device kernel attributes, set at pla
 cudaError_t stft_set_attributes();
 cudaError_t topk_set_attributes();
 
+// delay-and-sum SRP (das.cu): E16 from the phasor records, then the per-bin GEMM + sum of squares + argmax -> SRP keys
+int das_me(int M);
+bool das_active(const Plan& p, int F);     // plan has the operands and F fills the CTA pairs
+cudaError_t launch_das_bins(const Plan& p, const Band& b, int F, cudaStream_t s);
+cudaError_t launch_das(const Plan& p, const Band& b, int F, cudaStream_t s);
+cudaError_t das_set_attributes();
+
 // setup (float64, device)
+svdphat_status setup_das_operand(Plan& p, const double* h_delay_cls);
 svdphat_status setup_srp_operand(Plan& p, const double* d_tau_cls);
 svdphat_status setup_svd_operands(Plan& p, const double* d_tau_cls, int rank_D);
 

@@ -772,3 +772,58 @@ def test_one_cta_fallbacks():
     P_, Y_at = PP.svd_reference(fac, tau, x[keep], w.N)
     PP.compare(q[keep], s[keep], P_, Y_at, "1-CTA SVD")
     plan.close()
+
+
+@pytest.mark.parametrize("M,N,level,field,F", [(4, 256, 2, "far", 300), (12, 128, 2, "near", 531),
+                                               (16, 512, 3, "far", 300), (20, 64, 2, "far", 260),
+                                               (32, 128, 1, "near", 257)])
+def test_delay_and_sum_srp(M, N, level, field, F):
+    """NEXT-4: SRP-PHAT through the delay-and-sum form of eq. 5 (das.cu, forced with OPT_DAS: every K block width
+    ME = 8/16/32, ragged frame tiles, near and far field) against the oracle's eq. 9 (Y = Re{W X} in float64), and
+    DOA-identical to the plan's eq. 9 GEMM (OPT_NO_DAS) up to near-ties; then a band-limited call."""
+    from workloads import geometry as G
+    from workloads import scenes as SC
+    rng = np.random.default_rng(2000 + M + N)
+    mics = rng.uniform(-0.1, 0.1, (M, 3))
+    pts = G.icosphere(level)
+    if field == "near":
+        pts = pts * 1.5 + np.array([0.0, 0.1, 0.2])
+    hop = N // 2
+    L = (F - 1) * hop + N
+    src = pts[rng.integers(len(pts))]
+    audio = (SC.plane_wave_stream(rng, mics, 16000.0, 343.0, L, src / np.linalg.norm(src), 5.0)
+             if field == "far" else SC.point_source_stream(rng, mics, 16000.0, 343.0, L, src, 5.0)).astype(np.float32)
+    tau = srp.tdoa(mics, pts, 16000.0, 343.0, field)
+    x = srp.frames_to_x(srp.extract_frames(audio, F, M, N, L, hop))
+    d_audio = torch.from_numpy(audio).to(DEV)
+    st = torch.cuda.current_stream().cuda_stream
+    out = {}
+    for name, opt in (("das", S.OPT_DAS), ("w", S.OPT_NO_DAS)):
+        plan = S.Plan(mics, pts, 16000.0, 343.0, N, hop, field, methods=("srp",), max_frames=F, options=opt)
+        doa = torch.empty(F, dtype=torch.int32, device=DEV)
+        sc = torch.empty(F, dtype=torch.float32, device=DEV)
+        plan.profile_begin(16)
+        plan.localize("srp", d_audio, F, L, hop, doa, sc, st)
+        torch.cuda.synchronize()
+        stages = [n for n, _ in plan.profile_end()]
+        assert ("srp_das" in stages) == (name == "das"), stages
+        out[name] = (doa.cpu().numpy(), sc.cpu().numpy())
+        if name == "das":
+            k_lo, k_hi = N // 16, N // 2 - N // 8
+            dm = torch.empty(F, dtype=torch.int32, device=DEV)
+            sm = torch.empty(F, dtype=torch.float32, device=DEV)
+            plan.localize_masked("srp", d_audio, F, L, hop, k_lo, k_hi, None, 0, dm, sm, st)
+            torch.cuda.synchronize()
+            keep = np.zeros((F, N // 2 + 1), dtype=bool)
+            keep[:, k_lo:k_hi] = True
+            xm = srp.apply_tf_mask(x, M * (M - 1) // 2, keep)
+            qm, smv = dm.cpu().numpy(), sm.cpu().numpy()
+            kf = _check_degenerate(qm, smv, xm)
+            P_, Y_at = PP.srp_reference(tau, xm[kf], N)
+            PP.compare(qm[kf], smv[kf], P_, Y_at, f"M={M} N={N} das band")
+        plan.close()
+    q, s = out["das"]
+    keep = _check_degenerate(q, s, x)
+    P_, Y_at = PP.srp_reference(tau, x[keep], N)
+    st_ = PP.compare(q[keep], s[keep], P_, Y_at, f"M={M} N={N} das")
+    assert np.mean(out["das"][0] == out["w"][0]) >= 0.995, st_
