@@ -98,6 +98,9 @@ typedef struct {
                                   centrally symmetric in tau (class pairs tau_c' = -tau_c; R22)        */
     int32_t svd_rows;          /* rows of the SVD projection GEMM: 2*D (complex V, real-split) or D (real V when
                                   every class has its antipode; R22); 0 if SVD not planned             */
+    int32_t das_rows;          /* rows of the delay-and-sum SRP GEMM (2 per class: Re a_q, Im a_q; padded to 256);
+                                  0 if the plan has no delay-and-sum operand (M < 12 or SVDPHAT_OPT_NO_DAS)       */
+    int32_t das_me;            /* microphones of its contraction, padded to 8/16/32 (K = 2*das_me per bin)       */
 } svdphat_plan_info_t;
 
 /* Alg. 1 offline steps 1-3: TDOAs (eq. 1/2), W (eqs. 4, 8), SVD (eq. 10) with the rank rule

@@ -673,6 +673,8 @@ svdphat_status svdphat_plan_info(svdphat_plan_t plan, svdphat_plan_info_t* out) 
     out->setup_seconds = p.setup_seconds;
     out->srp_rows = (p.methods & SVDPHAT_METHOD_SRP) ? (p.fold ? p.fold_rows : p.Q_eff) : 0;
     out->svd_rows = (p.methods & SVDPHAT_METHOD_SVD) ? (p.svd_fold ? p.D : 2 * p.D) : 0;
+    out->das_rows = p.d_A16 ? p.das_rows : 0;
+    out->das_me = p.d_A16 ? p.das_me : 0;
     return SVDPHAT_OK;
 }
 
