@@ -68,14 +68,18 @@ typedef struct {
  *   NO_DAS        SRP-PHAT always through eq. 9's GEMM Y = Re{W X}, never through the delay-and-sum form of eq. 5
  *                 (Y_q = 1/2 sum_k |sum_m e_m[k] e^{j 2 pi k delta_qm / N}|^2 - n_k, tau_qij = delta_qi - delta_qj), which
  *                 the library uses by default for M >= 12 on batches that fill the GPU (NEXT-4);
- *   DAS           the delay-and-sum form for every M and every batch size. */
+ *   DAS           the delay-and-sum form for every M and every batch size;
+ *   DAS_FOLD      the antipodally folded delay-and-sum kernel also for 9..16 microphones (default only for 17..32):
+ *                 one (cos, sin) row pair per antipodal class pair (delta_q'm = -delta_qm + const, reading R22)
+ *                 against (Re e, Im e) frame columns, both classes' |a|^2 from the four real products. */
 enum {
     SVDPHAT_OPT_NO_SRP_FOLD = 1,
     SVDPHAT_OPT_NO_SVD_FOLD = 2,
     SVDPHAT_OPT_ONE_CTA_SRP = 4,
     SVDPHAT_OPT_ONE_CTA_PROJ = 8,
     SVDPHAT_OPT_NO_DAS = 16,
-    SVDPHAT_OPT_DAS = 32
+    SVDPHAT_OPT_DAS = 32,
+    SVDPHAT_OPT_DAS_FOLD = 64
 };
 
 typedef struct {

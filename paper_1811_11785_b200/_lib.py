@@ -20,7 +20,7 @@ STAGES = {1: "stft_phat", 2: "srp_gemm", 3: "svd_proj", 4: "svd_norm", 5: "svd_s
 _METHOD = {"srp": METHOD_SRP, "svd": METHOD_SVD, "both": METHOD_BOTH}
 DUMP_PHASORS, DUMP_Z, DUMP_CLASS_REP, DUMP_KEYS, DUMP_POWER = 1, 2, 3, 4, 5
 # svdphat_plan_desc.options: equivalent alternative kernels (tests / A-B measurements), 0 = product configuration
-OPT_NO_SRP_FOLD, OPT_NO_SVD_FOLD, OPT_ONE_CTA_SRP, OPT_ONE_CTA_PROJ, OPT_NO_DAS, OPT_DAS = 1, 2, 4, 8, 16, 32
+OPT_NO_SRP_FOLD, OPT_NO_SVD_FOLD, OPT_ONE_CTA_SRP, OPT_ONE_CTA_PROJ, OPT_NO_DAS, OPT_DAS, OPT_DAS_FOLD = 1, 2, 4, 8, 16, 32, 64
 
 
 class PlanDesc(C.Structure):

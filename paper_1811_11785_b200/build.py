@@ -32,12 +32,27 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def _compile(src: str) -> tuple[str, str]:
+def _obj_fresh(src: str, obj: str) -> bool:
+    """The object is newer than its source, the shared headers and the build flags (this file)."""
+    if not os.path.exists(obj):
+        return False
+    deps = [os.path.join(CSRC, src)] + [os.path.join(CSRC, h) for h in HEADERS] + \
+        [os.path.join(ROOT, "include", "svdphat.h"), os.path.abspath(__file__)]
+    t = os.path.getmtime(obj)
+    return all(os.path.getmtime(d) <= t for d in deps)
+
+
+def _compile(src: str, force: bool = False) -> tuple[str, str]:
     obj = os.path.join(BUILD, os.path.splitext(src)[0] + ".o")
+    log = obj + ".ptxas.log"
+    if not force and _obj_fresh(src, obj) and os.path.exists(log):
+        return obj, open(log).read()
     cmd = [NVCC, *ARCH, *FLAGS, "-c", os.path.join(CSRC, src), "-o", obj]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr[-6000:]}")
+    with open(log, "w") as f:
+        f.write(r.stderr)
     return obj, r.stderr
 
 
@@ -46,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return OUT
     os.makedirs(BUILD, exist_ok=True)
     with cf.ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
-        res = list(ex.map(_compile, SOURCES))
+        res = list(ex.map(lambda f: _compile(f, force), SOURCES))
     objs = [o for o, _ in res]
     with open(os.path.join(BUILD, "ptxas.log"), "w") as f:
         for _, log in res:

@@ -166,7 +166,7 @@ static svdphat_status validate(const svdphat_plan_desc* d) {
     if (d->rank_D < 0) return fail(SVDPHAT_INVALID_ARG, "rank_D must be >= 0");
     if (d->max_frames < 0 || d->max_frames > (1ll << 26)) return fail(SVDPHAT_INVALID_ARG, "max_frames out of range");
     if (d->options & ~(SVDPHAT_OPT_NO_SRP_FOLD | SVDPHAT_OPT_NO_SVD_FOLD | SVDPHAT_OPT_ONE_CTA_SRP |
-                       SVDPHAT_OPT_ONE_CTA_PROJ | SVDPHAT_OPT_NO_DAS | SVDPHAT_OPT_DAS))
+                       SVDPHAT_OPT_ONE_CTA_PROJ | SVDPHAT_OPT_NO_DAS | SVDPHAT_OPT_DAS | SVDPHAT_OPT_DAS_FOLD))
         return fail(SVDPHAT_INVALID_ARG, "unknown option bits");
     for (int i = 0; i < 3 * d->M; ++i)
         if (!std::isfinite(d->mic_xyz[i])) return fail(SVDPHAT_INVALID_ARG, "non-finite microphone coordinate");
@@ -417,6 +417,13 @@ static svdphat_status plan_create_impl(const svdphat_plan_desc* d, svdphat_plan_
     p.svd_fold = !(p.options & SVDPHAT_OPT_NO_SVD_FOLD) && p.pair_proj && (p.methods & SVDPHAT_METHOD_SVD) &&
                  few_rows && all_paired;
     p.fold_rows = (int)fold_m.size();
+    // delay-and-sum SRP (das.cu) for M >= 12, where its (M-1)/4-fold saving in MMA work beats eq. 9's GEMM; folded
+    // on centrally symmetric grids (antipodal class pairs, reading R22) for 17..32 microphones (cfg4: 13.0 -> 11.0
+    // ms; at 16 microphones the unfolded kernel measured faster, 8.7 vs 9.4 ms at cfg3), or when forced
+    const bool use_das = (p.methods & SVDPHAT_METHOD_SRP) &&
+                         ((p.options & SVDPHAT_OPT_DAS) || (!(p.options & SVDPHAT_OPT_NO_DAS) && p.M >= 12));
+    p.das_fold = use_das && few_rows && !(p.options & SVDPHAT_OPT_NO_SRP_FOLD) &&
+                 (das_me(p.M) == 32 || (das_me(p.M) == 16 && (p.options & SVDPHAT_OPT_DAS_FOLD)));
     p.spc_F = 2 * ((p.L.U + 15) / 16);
     p.K_F = (int64_t)p.L.n_chunks * p.spc_F * 64;
     p.spc_P = (p.L.U + 15) / 16;
@@ -482,7 +489,7 @@ static svdphat_status plan_create_impl(const svdphat_plan_desc* d, svdphat_plan_
     SVD_CUDA_TRY(cudaMalloc(&d_tau, tau_cls.size() * 8));
     std::unique_ptr<double, decltype(&cudaFree)> tau_guard(d_tau, &cudaFree);
     SVD_CUDA_TRY(cudaMemcpy(d_tau, tau_cls.data(), tau_cls.size() * 8, cudaMemcpyHostToDevice));
-    if (p.fold) {
+    if (p.fold || p.das_fold) {
         std::vector<int> fc(fold_m);
         fc.insert(fc.end(), fold_p.begin(), fold_p.end());
         SVD_CUDA_TRY(cudaMalloc(&p.d_fold_cls, fc.size() * sizeof(int)));
@@ -539,9 +546,15 @@ static svdphat_status plan_create_impl(const svdphat_plan_desc* d, svdphat_plan_
         if (st != SVDPHAT_OK) return st;
         if (!encode_2d(&p.tm_W, p.d_W16, p.W_rows, p.K_W, 128))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(W) failed");
-        // delay-and-sum SRP (das.cu) for M >= 12, where its (M-1)/4-fold saving in MMA work beats eq. 9's GEMM
-        const bool use_das = (p.options & SVDPHAT_OPT_DAS) || (!(p.options & SVDPHAT_OPT_NO_DAS) && p.M >= 12);
-        if (use_das) {
+        if (p.das_fold) {
+            std::vector<double> dfold((size_t)p.fold_rows * M);
+            for (int r = 0; r < p.fold_rows; ++r)
+                std::memcpy(&dfold[(size_t)r * M], &delay[(size_t)p.rep_q[fold_m[r]] * M], (size_t)M * 8);
+            st = setup_das_fold_operand(p, dfold.data());
+            if (st != SVDPHAT_OK) return st;
+            if (!encode_2d_rows(&p.tm_A, p.d_A16, (int64_t)p.L.n_chunks * p.das_rows, 64, 128))
+                return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(A16) failed");
+        } else if (use_das) {
             std::vector<double> dcls((size_t)p.Q_eff * M);
             for (int c = 0; c < p.Q_eff; ++c)
                 std::memcpy(&dcls[(size_t)c * M], &delay[(size_t)p.rep_q[c] * M], (size_t)M * 8);
@@ -578,10 +591,13 @@ static svdphat_status plan_create_impl(const svdphat_plan_desc* d, svdphat_plan_
     SVD_CUDA_TRY(cudaMalloc(&p.d_keys, 3 * Fp * sizeof(unsigned long long)));
     p.bytes_ws = bytes_P16 + 3 * Fp * 8;
     if (p.d_A16) {
-        const int64_t bytes_E16 = (int64_t)p.Kb * Fp * 2 * p.das_me * 2;
+        // folded: [n_chunks][2 F_pad][64 halves] (Re row, Im row per frame); else [Kb][F_pad][2 das_me]
+        const int64_t e_rows = p.das_fold ? (int64_t)p.L.n_chunks * 2 * Fp : (int64_t)p.Kb * Fp;
+        const int e_cols = p.das_fold ? 64 : 2 * p.das_me;
+        const int64_t bytes_E16 = e_rows * e_cols * 2;
         SVD_CUDA_TRY(cudaMalloc(&p.d_E16, bytes_E16));
         SVD_CUDA_TRY(cudaMemset(p.d_E16, 0, bytes_E16));
-        if (!encode_2d_rows(&p.tm_E, p.d_E16, (int64_t)p.Kb * Fp, 2 * p.das_me, 128))
+        if (!encode_2d_rows(&p.tm_E, p.d_E16, e_rows, e_cols, 128))
             return fail(SVDPHAT_CUDA, "cuTensorMapEncodeTiled(E16) failed");
         p.bytes_ws += bytes_E16;
     }

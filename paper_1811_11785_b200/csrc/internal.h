@@ -109,7 +109,11 @@ struct Plan {
     // delay-and-sum SRP (das.cu, NEXT-4): per-bin steering rows A16[Kb][das_rows][2 das_me] (Re / Im rows of each
     // class) and the frames' phasors re-laid per bin, E16[Kb][F_pad][2 das_me]
     int das_me = 0;               // microphones per K block (8, 16, 32): K = 2 das_me per bin
-    int das_rows = 0;             // 2 Q_eff rounded up to 256
+    int das_rows = 0;             // 2 Q_eff rounded up to 256 (folded: 2 fold_rows rounded up to 256)
+    // folded delay-and-sum (centrally symmetric grids, das_me >= 16): one (cos, sin) row pair per antipodal class
+    // pair, K = das_me per bin, frames as (Re e, Im e) column pairs; operands per bin chunk, one 128-byte row holding
+    // the chunk's bins: A16[n_chunks][das_rows][bpc * das_me], E16[n_chunks][2 F_pad][bpc * das_me]
+    bool das_fold = false;
     __half* d_A16 = nullptr;
     __half* d_E16 = nullptr;
     int64_t bytes_W = 0, bytes_V = 0, bytes_R = 0, bytes_ws = 0, bytes_A = 0;
@@ -221,6 +225,8 @@ cudaError_t das_set_attributes();
 
 // setup (float64, device)
 svdphat_status setup_das_operand(Plan& p, const double* h_delay_cls);
+// folded form: h_delay_fold [fold_rows][M] = delays of each fold row's first class (d_fold_cls[0][r])
+svdphat_status setup_das_fold_operand(Plan& p, const double* h_delay_fold);
 svdphat_status setup_srp_operand(Plan& p, const double* d_tau_cls);
 svdphat_status setup_svd_operands(Plan& p, const double* d_tau_cls, int rank_D);
 

@@ -77,7 +77,7 @@ BAD = [
     dict(methods=()),
     dict(max_frames=-1),
     dict(rank_D=-2),
-    dict(options=64),                                  # unknown option bit
+    dict(options=128),                                 # unknown option bit
 ]
 
 

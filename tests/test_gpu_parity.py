@@ -774,13 +774,15 @@ def test_one_cta_fallbacks():
     plan.close()
 
 
-@pytest.mark.parametrize("M,N,level,field,F", [(4, 256, 2, "far", 300), (12, 128, 2, "near", 531),
-                                               (16, 512, 3, "far", 300), (20, 64, 2, "far", 260),
-                                               (32, 128, 1, "near", 257)])
-def test_delay_and_sum_srp(M, N, level, field, F):
+@pytest.mark.parametrize("M,N,level,field,F,fold", [(4, 256, 2, "far", 300, False), (12, 128, 2, "near", 531, False),
+                                                    (16, 512, 3, "far", 300, False), (20, 64, 2, "far", 260, False),
+                                                    (32, 128, 1, "near", 257, False), (12, 256, 2, "far", 301, True),
+                                                    (16, 512, 3, "far", 300, True)])
+def test_delay_and_sum_srp(M, N, level, field, F, fold):
     """NEXT-4: SRP-PHAT through the delay-and-sum form of eq. 5 (das.cu, forced with OPT_DAS: every K block width
-    ME = 8/16/32, ragged frame tiles, near and far field) against the oracle's eq. 9 (Y = Re{W X} in float64), and
-    DOA-identical to the plan's eq. 9 GEMM (OPT_NO_DAS) up to near-ties; then a band-limited call."""
+    ME = 8/16/32, ragged frame tiles, near and far field; the antipodally folded kernel on the far-field icospheres
+    for 17..32 microphones by default and for 9..16 with OPT_DAS_FOLD) against the oracle's eq. 9 (Y = Re{W X} in
+    float64), and DOA-identical to the plan's eq. 9 GEMM (OPT_NO_DAS) up to near-ties; then a band-limited call."""
     from workloads import geometry as G
     from workloads import scenes as SC
     rng = np.random.default_rng(2000 + M + N)
@@ -798,7 +800,7 @@ def test_delay_and_sum_srp(M, N, level, field, F):
     d_audio = torch.from_numpy(audio).to(DEV)
     st = torch.cuda.current_stream().cuda_stream
     out = {}
-    for name, opt in (("das", S.OPT_DAS), ("w", S.OPT_NO_DAS)):
+    for name, opt in (("das", S.OPT_DAS | (S.OPT_DAS_FOLD if fold else 0)), ("w", S.OPT_NO_DAS)):
         plan = S.Plan(mics, pts, 16000.0, 343.0, N, hop, field, methods=("srp",), max_frames=F, options=opt)
         doa = torch.empty(F, dtype=torch.int32, device=DEV)
         sc = torch.empty(F, dtype=torch.float32, device=DEV)
