@@ -145,23 +145,14 @@ __device__ __forceinline__ void das_epi_region(float* s, uint32_t taddr, uint32_
     wait_u32(tf, parity);
     tc_fence_after();
     uint32_t va[16], vb[16];
-#if defined(DAS_EXP) && DAS_EXP == 1
-#pragma unroll
-    for (int i = 0; i < 16; ++i) va[i] = vb[i] = taddr;
-#else
     tmem_ld16x256_x4(taddr, va);
     tmem_ld16x256_x4(taddr + (16u << 16), vb);
     tmem_ld_wait();
-#endif
     tc_fence_before();
     asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e mbarrier.arrive.shared::cluster.b64 _, [%0];\n\t}" ::"r"(te)
                  : "memory");
-#if defined(DAS_EXP) && DAS_EXP == 2
-    s[0] += __uint_as_float(va[0] ^ vb[15]);
-#else
     sumsq_c8(s, va);
     sumsq_c8(s + 8, vb);
-#endif
 }
 
 template <int NK>
@@ -250,10 +241,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DAS_THREADS, 1)
                         const int r = 2 * acc + hf;
                         mbar_wait(&tempty[r], acc_phase ^ 1);
                         tc_fence_after();
-#if !(defined(DAS_EXP) && DAS_EXP == 3)
                         das_mma<C::NK>(tmem_base + (uint32_t)(r * DAS_RCOLS), a_lo0 + so, b_lo0 + so + hf * HALF_B,
                                        C::HI, idesc);
-#endif
                         umma_commit_2sm_warp(&tfull[r], 0x3);
                     }
                     umma_commit_2sm_warp(&empty[stage], 0x3);
@@ -378,6 +367,17 @@ constexpr int DASF_BF = 128;          // frames per pair unit (2 columns each: N
 constexpr int DASF_EW = 16;
 constexpr int DASF_THREADS = 32 * (2 + DASF_EW);
 
+#ifdef DAS_TRACE   // dev-only latency trace (tools/das_trace.py): [0] MMA issue, [1] epilogue wake, [2] epilogue release
+__device__ long long g_das_trace[3][8192];
+extern "C" int svdphat_dev_das_trace(long long* out, int n) {
+    return (int)cudaMemcpyFromSymbol(out, g_das_trace, (size_t)n * sizeof(long long));
+}
+#define DAS_TRACE_REC(i, s) \
+    if ((s) < 8192) g_das_trace[i][s] = clock64();
+#else
+#define DAS_TRACE_REC(i, s)
+#endif
+
 struct DasFParams {
     int F;
     int64_t F_pad;
@@ -424,9 +424,11 @@ __device__ __forceinline__ void fold_acc_load(float2* w, const uint32_t (&v)[16]
 // quarter) and frame block b of the warp's 32 columns: two loads, the region released once both have landed, then
 // the sums.
 __device__ __forceinline__ void dasf_epi_region(float2* w, uint32_t taddr, uint32_t tf, uint32_t te,
-                                                uint32_t parity) {
+                                                uint32_t parity, int& dbg) {
     wait_u32(tf, parity);
     tc_fence_after();
+    const bool rec = blockIdx.x == 0 && threadIdx.x == 64;
+    if (rec) { DAS_TRACE_REC(1, dbg) }
     uint32_t va[16], vb[16];
     tmem_ld16x256_x4(taddr, va);
     tmem_ld16x256_x4(taddr + (16u << 16), vb);
@@ -434,6 +436,8 @@ __device__ __forceinline__ void dasf_epi_region(float2* w, uint32_t taddr, uint3
     tc_fence_before();
     asm volatile("{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t@e mbarrier.arrive.shared::cluster.b64 _, [%0];\n\t}" ::"r"(te)
                  : "memory");
+    if (rec) { DAS_TRACE_REC(2, dbg) }
+    ++dbg;
     fold_acc_load(w, va);
     fold_acc_load(w + 4, vb);
 }
@@ -503,7 +507,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DASF_THREADS, 1)
             const uint32_t idesc = umma_idesc_f16(256, DAS_RCOLS);
             const uint32_t a_lo0 = umma_desc_lo(smem_u32(smem)), b_lo0 = umma_desc_lo(smem_u32(smem + C::TILE));
             constexpr uint32_t HALF_B = (uint32_t)((64 * 128) >> 4);   // B rows 64..127 (frames 32..63 of the CTA)
-            int stage = 0, acc = 0;
+            int stage = 0, acc = 0, dbg_step = 0;
             uint32_t phase = 0, acc_phase = 0;
             for (int t = pair; t < units; t += n_pairs) {
                 for (int c = p.c_lo; c < p.c_hi; ++c) {
@@ -517,6 +521,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DASF_THREADS, 1)
                             const int r = 2 * acc + hf;
                             mbar_wait(&tempty[r], acc_phase ^ 1);
                             tc_fence_after();
+                            if (blockIdx.x == 0 && lane == 0) { DAS_TRACE_REC(0, dbg_step) }
+                            ++dbg_step;
                             das_mma<C::NK>(tmem_base + (uint32_t)(r * DAS_RCOLS), a_lo0 + so + ko,
                                            b_lo0 + so + hf * HALF_B + ko, C::HI, idesc);
                             umma_commit_2sm_warp(&tfull[r], 0x3);
@@ -541,7 +547,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DASF_THREADS, 1)
         const uint32_t tb = tmem_base + ((uint32_t)(g * 32) << 16) + (uint32_t)(h * 32);
         const uint32_t te = mapa_u32(smem_u32(&tempty[0]), 0);
         const uint32_t tf = smem_u32(&tfull[0]);
-        int acc = 0;
+        int acc = 0, dbg = 0;
         uint32_t ph = 0;
         float2 w[16];                      // [hf][u][b][q, q']: partial sums over a frame pair
         for (int t = pair; t < units; t += n_pairs) {
@@ -551,22 +557,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(DASF_THREADS, 1)
             for (int i = 0; i < 16; ++i) w[i] = make_float2(0.f, 0.f);
             int k = 0;
             if (acc == 1 && k < nbins) {
-                dasf_epi_region(w, tb + 2 * DAS_RCOLS, tf + 16, te + 16, ph);
-                dasf_epi_region(w + 8, tb + 3 * DAS_RCOLS, tf + 24, te + 24, ph);
+                dasf_epi_region(w, tb + 2 * DAS_RCOLS, tf + 16, te + 16, ph, dbg);
+                dasf_epi_region(w + 8, tb + 3 * DAS_RCOLS, tf + 24, te + 24, ph, dbg);
                 ph ^= 1;
                 acc = 0;
                 ++k;
             }
             for (; k + 1 < nbins; k += 2) {
-                dasf_epi_region(w, tb, tf, te, ph);
-                dasf_epi_region(w + 8, tb + DAS_RCOLS, tf + 8, te + 8, ph);
-                dasf_epi_region(w, tb + 2 * DAS_RCOLS, tf + 16, te + 16, ph);
-                dasf_epi_region(w + 8, tb + 3 * DAS_RCOLS, tf + 24, te + 24, ph);
+                dasf_epi_region(w, tb, tf, te, ph, dbg);
+                dasf_epi_region(w + 8, tb + DAS_RCOLS, tf + 8, te + 8, ph, dbg);
+                dasf_epi_region(w, tb + 2 * DAS_RCOLS, tf + 16, te + 16, ph, dbg);
+                dasf_epi_region(w + 8, tb + 3 * DAS_RCOLS, tf + 24, te + 24, ph, dbg);
                 ph ^= 1;
             }
             if (k < nbins) {
-                dasf_epi_region(w, tb, tf, te, ph);
-                dasf_epi_region(w + 8, tb + DAS_RCOLS, tf + 8, te + 8, ph);
+                dasf_epi_region(w, tb, tf, te, ph, dbg);
+                dasf_epi_region(w + 8, tb + DAS_RCOLS, tf + 8, te + 8, ph, dbg);
                 acc = 1;
             }
             // classes of the thread's two class pairs
