@@ -325,7 +325,10 @@ def roofline(info, w, F, stage_ms, clocks) -> dict:
         tkey = "srp_das_dram_bytes_per_launch"
     elif dom == "srp_gemm":
         flops = 4.0 * info["srp_rows"] * info["PK"] * F
-        executed = 4.0 * (-(-info["srp_rows"] // 256) * 256) * info["gemm_k"] / 2 * F_exec
+        # executed: the W rows of the tiles the GEMM runs (BOTH calls skip the tail tile, whose rows ride in the SVD
+        # projection) x the padded contraction (fold layout: 120 units per bin chunk padded to 128) x 256-frame tiles
+        rows_exec = info["srp_gemm_rows"] - (256 if info["srp_tail_rows"] > 0 else 0)
+        executed = 2.0 * rows_exec * info["srp_gemm_k"] * F_exec
         kern, basis = "srp_gemm (gemm2_kernel, CTA pairs)", f"4*srp_rows*PK*F, srp_rows={info['srp_rows']}"
         extra, tkey = {}, "srp_gemm_dram_bytes_per_launch"
     else:

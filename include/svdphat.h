@@ -67,7 +67,7 @@ typedef struct {
  *   ONE_CTA_PROJ  1-CTA V-on-M projection GEMM instead of the frames-on-M CTA-pair kernel (implies NO_SVD_FOLD);
  *   NO_DAS        SRP-PHAT always through eq. 9's GEMM Y = Re{W X}, never through the delay-and-sum form of eq. 5
  *                 (Y_q = 1/2 sum_k |sum_m e_m[k] e^{j 2 pi k delta_qm / N}|^2 - n_k, tau_qij = delta_qi - delta_qj), which
- *                 the library uses by default for M >= 12 on batches that fill the GPU (NEXT-4);
+ *                 the library uses by default for M >= 17 on batches that fill the GPU (NEXT-4);
  *   DAS           the delay-and-sum form for every M and every batch size;
  *   DAS_FOLD      the antipodally folded delay-and-sum kernel also for 9..16 microphones (default only for 17..32):
  *                 one (cos, sin) row pair per antipodal class pair (delta_q'm = -delta_qm + const, reading R22)
@@ -105,6 +105,9 @@ typedef struct {
     int32_t das_rows;          /* rows of the delay-and-sum SRP GEMM (2 per class: Re a_q, Im a_q; padded to 256);
                                   0 if the plan has no delay-and-sum operand (M < 12 or SVDPHAT_OPT_NO_DAS)       */
     int32_t das_me;            /* microphones of its contraction, padded to 8/16/32 (K = 2*das_me per bin)       */
+    int64_t srp_gemm_k;        /* contraction length the eq. 9 SRP GEMM executes (padded, fold layout if folded)  */
+    int32_t srp_gemm_rows;     /* W rows it holds (256-row tiles)                                               */
+    int32_t srp_tail_rows;     /* fold rows past the last full tile that BOTH calls score through the projection */
 } svdphat_plan_info_t;
 
 /* Alg. 1 offline steps 1-3: TDOAs (eq. 1/2), W (eqs. 4, 8), SVD (eq. 10) with the rank rule

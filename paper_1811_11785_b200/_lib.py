@@ -37,7 +37,8 @@ class PlanInfo(C.Structure):
                 ("max_frames", C.c_int64), ("bytes_W", C.c_int64), ("bytes_V", C.c_int64), ("bytes_R", C.c_int64),
                 ("bytes_workspace", C.c_int64), ("setup_seconds", C.c_double),
                 ("srp_rows", C.c_int32), ("svd_rows", C.c_int32), ("das_rows", C.c_int32),
-                ("das_me", C.c_int32)]
+                ("das_me", C.c_int32), ("srp_gemm_k", C.c_int64), ("srp_gemm_rows", C.c_int32),
+                ("srp_tail_rows", C.c_int32)]
 
 
 def _load() -> C.CDLL:

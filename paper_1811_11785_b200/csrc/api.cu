@@ -417,11 +417,13 @@ static svdphat_status plan_create_impl(const svdphat_plan_desc* d, svdphat_plan_
     p.svd_fold = !(p.options & SVDPHAT_OPT_NO_SVD_FOLD) && p.pair_proj && (p.methods & SVDPHAT_METHOD_SVD) &&
                  few_rows && all_paired;
     p.fold_rows = (int)fold_m.size();
-    // delay-and-sum SRP (das.cu) for M >= 12, where its (M-1)/4-fold saving in MMA work beats eq. 9's GEMM; folded
-    // on centrally symmetric grids (antipodal class pairs, reading R22) for 17..32 microphones (cfg4: 13.0 -> 11.0
-    // ms; at 16 microphones the unfolded kernel measured faster, 8.7 vs 9.4 ms at cfg3), or when forced
+    // delay-and-sum SRP (das.cu) for M >= 17, where its (M-1)/4-fold saving in MMA work beats eq. 9's GEMM (cfg4
+    // BOTH: 24.3 vs 50.2 ms); at 16 microphones the two SRP paths are within 3% alone and eq. 9's GEMM wins the BOTH
+    // call (cfg3: 10.2-10.5 vs 11.0-11.1 ms, profiles/r02/ab_both_das_vs_eq9.log) because the SVD chain overlaps it.  Folded on
+    // centrally symmetric grids (antipodal class pairs, reading R22) for 17..32 microphones (cfg4 SRP 13.0 -> 11.0
+    // ms), or when forced
     const bool use_das = (p.methods & SVDPHAT_METHOD_SRP) &&
-                         ((p.options & SVDPHAT_OPT_DAS) || (!(p.options & SVDPHAT_OPT_NO_DAS) && p.M >= 12));
+                         ((p.options & SVDPHAT_OPT_DAS) || (!(p.options & SVDPHAT_OPT_NO_DAS) && p.M >= 17));
     p.das_fold = use_das && few_rows && !(p.options & SVDPHAT_OPT_NO_SRP_FOLD) &&
                  (das_me(p.M) == 32 || (das_me(p.M) == 16 && (p.options & SVDPHAT_OPT_DAS_FOLD)));
     p.spc_F = 2 * ((p.L.U + 15) / 16);
@@ -691,6 +693,9 @@ svdphat_status svdphat_plan_info(svdphat_plan_t plan, svdphat_plan_info_t* out) 
     out->svd_rows = (p.methods & SVDPHAT_METHOD_SVD) ? (p.svd_fold ? p.D : 2 * p.D) : 0;
     out->das_rows = p.d_A16 ? p.das_rows : 0;
     out->das_me = p.d_A16 ? p.das_me : 0;
+    out->srp_gemm_k = (p.methods & SVDPHAT_METHOD_SRP) ? p.K_W : 0;
+    out->srp_gemm_rows = (p.methods & SVDPHAT_METHOD_SRP) ? p.W_rows : 0;
+    out->srp_tail_rows = p.tail_n;
     return SVDPHAT_OK;
 }
 
