@@ -298,7 +298,7 @@ def _p16_bytes(info, w, F) -> float:
 
 
 def roofline(info, w, F, stage_ms, clocks) -> dict:
-    """Roofline of the dominant kernel of the timed step (the stage with the largest average event time).
+    """Roofline of the dominant kernel of the timed step (the SRP stage: 80-90% of the step's kernel time, ncu launch list).
 
     Delay-and-sum SRP (das_kernel, NEXT-4): per (class, bin, frame) a_q[k] = sum_m e_m e^{j phi_qm} is M
     complex MACs = 8 M flops, so 8 Q_classes M K F algorithmic flops per launch; the kernel executes
@@ -307,7 +307,9 @@ def roofline(info, w, F, stage_ms, clocks) -> dict:
     Eq. 9 GEMM (srp_gemm): 4 srp_rows PK F (SURVEY §8d's 4 Q PK per frame on the rows the GEMM executes, R11/R22).
     Peak: the measured burst dense FP16/BF16 rate (a kernel of a few ms timed inside a sub-second region)."""
     pk = _peaks()
-    dom = max(stage_ms, key=stage_ms.get)
+    # the SRP stage: in a BOTH step the SVD chain runs on a low-priority stream beside it, so an SVD stage's event
+    # time includes waiting for the SMs the SRP kernel holds and is not a kernel duration
+    dom = next((k for k in ("srp_das", "srp_gemm") if k in stage_ms), max(stage_ms, key=stage_ms.get))
     ms = stage_ms[dom]
     F_exec = -(-F // 256) * 256
     traffic = _ncu_traffic()
