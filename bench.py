@@ -328,9 +328,11 @@ def roofline(info, w, F, stage_ms, clocks) -> dict:
     elif dom == "srp_gemm":
         flops = 4.0 * info["srp_rows"] * info["PK"] * F
         # executed: the W rows of the tiles the GEMM runs (BOTH calls skip the tail tile, whose rows ride in the SVD
-        # projection) x the padded contraction (fold layout: 120 units per bin chunk padded to 128) x 256-frame tiles
+        # projection) x the contraction the MMAs cover x 256-frame tiles.  The fold layout stores 128 unit slots per
+        # bin chunk for 120 pairs (srp_gemm_k, what TMA streams), but the issuer skips the two empty K steps of each
+        # chunk's last slab pair (kHalfPair, gemm_tc.cu), so the MMAs cover gemm_k = chunks x units x 8 halves
         rows_exec = info["srp_gemm_rows"] - (256 if info["srp_tail_rows"] > 0 else 0)
-        executed = 2.0 * rows_exec * info["srp_gemm_k"] * F_exec
+        executed = 2.0 * rows_exec * info["gemm_k"] * F_exec
         kern, basis = "srp_gemm (gemm2_kernel, CTA pairs)", f"4*srp_rows*PK*F, srp_rows={info['srp_rows']}"
         extra, tkey = {}, "srp_gemm_dram_bytes_per_launch"
     else:
@@ -431,6 +433,30 @@ def main() -> None:
         if dist is not None:
             dist.barrier()
 
+    def timed(method, n, warm=3):
+        for _ in range(warm):
+            step(method)
+        torch.cuda.synchronize(dev)
+        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        x0.record(stream)
+        for _ in range(n):
+            step(method)
+        x1.record(stream)
+        torch.cuda.synchronize(dev)
+        return x0.elapsed_time(x1) / n
+
+    # ---------------------------------------------------------------- SVD-PHAT alone (method=svd), with stage events
+    # Timed before the SRP legs: inside the "both" step the SVD chain shares the SMs with the SRP GEMM, and right after
+    # a run of SRP GEMMs the board sits at its power cap with the SM clock ~30% down for a while (r02: every SVD kernel
+    # measured 1.23-1.33x slower there), which an SVD-only caller never sees.
+    n_svd = max(20, 2 * a.steps)
+    plan.profile_begin(8 * n_svd + 16)
+    svd_ms = timed("svd", n_svd)
+    svd_stages: dict[str, list[float]] = {}
+    for name, ms in plan.profile_end():
+        svd_stages.setdefault(name, []).append(ms)
+    svd_stage_ms = {k: float(np.mean(v)) for k, v in svd_stages.items()}
+
     for _ in range(max(3, a.warmup)):
         step()
     torch.cuda.synchronize(dev)
@@ -458,27 +484,8 @@ def main() -> None:
     stage_ms = {k: float(np.mean(v)) for k, v in stages.items()}
     launches = len(prof)
 
-    # ---------------------------------------------------------------- per-method throughput (same protocol)
-    def timed(method, n):
-        for _ in range(2):
-            step(method)
-        torch.cuda.synchronize(dev)
-        x0, x1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        x0.record(stream)
-        for _ in range(n):
-            step(method)
-        x1.record(stream)
-        torch.cuda.synchronize(dev)
-        return x0.elapsed_time(x1) / n
-    srp_ms = timed("srp", max(3, a.steps // 2))
-    # the SVD chain alone, with its stage events: inside the "both" step the projection shares the SMs with the
-    # SRP GEMM, so its own roofline is measured here
-    plan.profile_begin(8 * max(3, a.steps // 2) + 16)
-    svd_ms = timed("svd", max(3, a.steps // 2))
-    svd_stages: dict[str, list[float]] = {}
-    for name, ms in plan.profile_end():
-        svd_stages.setdefault(name, []).append(ms)
-    svd_stage_ms = {k: float(np.mean(v)) for k, v in svd_stages.items()}
+    # ---------------------------------------------------------------- SRP-PHAT alone (same protocol)
+    srp_ms = timed("srp", max(3, a.steps // 2), warm=2)
 
     # ---------------------------------------------------------------- end to end through the host-buffer C-ABI
     # svdphat_submit_host: every step uploads its 655 MB of pinned float32 audio, localises and downloads the

@@ -258,22 +258,28 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
                             if (f0 + jj < p.F) Zs[(int64_t)(f0 + jj) * p.ldz + row] = __uint_as_float(r[jj]);
                         }
                     }
-                } else {
-                    unsigned long long k[32];
+                } else if (MODE == 2) {
+                    // FP16 search: only the frame's running FP16 maximum (the base of the candidate threshold) and the
+                    // candidate rows leave the tile; the class of that maximum is never used (rescore_kernel decides
+                    // among the candidates in FP32), so the column maximum over the warp's 32 rows is one
+                    // redux.sync.max.f32 per frame instead of a u64 key transpose (ncu r02: the key epilogue issued
+                    // ~3500 instructions per warp and tile, 21k cycles per tile against 5k of MMA; NaN inputs are
+                    // ignored by the reduction and fail the >= below).
+                    float mx = -INFINITY;
 #pragma unroll
                     for (int jj = 0; jj < 32; ++jj) {
-                        const float v = __uint_as_float(r[jj]);
-                        k[jj] = (row_ok && v == v) ? make_key(v, (uint32_t)row) : 0ull;
+                        const float v = row_ok ? __uint_as_float(r[jj]) : -INFINITY;
+                        const float m = warp_max_f32(v);
+                        mx = lane == jj ? m : mx;
                     }
-                    const unsigned long long best = transpose_max32(k, lane);
-                    if (fok && best != 0ull) atomicMax(&p.keys[f0 + lane], best);
-                    if (MODE == 2) {
-                        // candidates of the exact rescore: rows within SEARCH_TAU of the running FP16 maximum.  The
-                        // exact argmax q* has s16(q*) >= max16 - 2e >= running - SEARCH_TAU (e: FP16 error bound).
-                        const unsigned long long run = prev > best ? prev : best;
-                        const float thr = (fok && run) ? o2f((uint32_t)(run >> 32)) - SEARCH_TAU : INFINITY;
-                        const bool any = best != 0ull && o2f((uint32_t)(best >> 32)) >= thr;
-                        const uint32_t mask = __ballot_sync(0xffffffffu, any);
+                    const float prev_f = prev ? o2f((uint32_t)(prev >> 32)) : -INFINITY;
+                    // candidates of the exact rescore: rows within SEARCH_TAU of the running FP16 maximum.  The exact
+                    // argmax q* has s16(q*) >= max16 - 2e >= running - SEARCH_TAU (e: FP16 error bound).
+                    const float thr = fmaxf(prev_f, mx) - SEARCH_TAU;
+                    const bool any = fok && mx > -INFINITY && mx >= thr;
+                    if (any && mx > prev_f) atomicMax(&p.keys[f0 + lane], make_key(mx, 0u));
+                    const uint32_t mask = __ballot_sync(0xffffffffu, any);
+                    if (mask) {
 #pragma unroll
                         for (int jj = 0; jj < 32; ++jj) {
                             if (mask & (1u << jj)) {
@@ -287,6 +293,15 @@ __global__ void __launch_bounds__(32 * (6 + NUM_PRODUCER_WARPS), 1)
                             }
                         }
                     }
+                } else {
+                    unsigned long long k[32];
+#pragma unroll
+                    for (int jj = 0; jj < 32; ++jj) {
+                        const float v = __uint_as_float(r[jj]);
+                        k[jj] = (row_ok && v == v) ? make_key(v, (uint32_t)row) : 0ull;
+                    }
+                    const unsigned long long best = transpose_max32(k, lane);
+                    if (fok && best != 0ull) atomicMax(&p.keys[f0 + lane], best);
                 }
             }
             tc_fence_before();

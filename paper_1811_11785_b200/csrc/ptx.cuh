@@ -294,6 +294,14 @@ __device__ __forceinline__ unsigned long long make_key(float v, uint32_t idx) {
     return ((unsigned long long)f2o(v) << 32) | (unsigned long long)(0xFFFFFFFFu - idx);
 }
 
+// maximum of v over the 32 lanes of the (converged) warp, in every lane: one CREDUX.MAX.F32 (sm_100a); NaN inputs are
+// ignored unless every lane holds one
+__device__ __forceinline__ float warp_max_f32(float v) {
+    float m;
+    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(m) : "f"(v));
+    return m;
+}
+
 // u64 max-reduce of 32 columns across the 32 lanes of a warp; afterwards lane l holds column l's maximum.
 __device__ __forceinline__ unsigned long long transpose_max32(unsigned long long (&k)[32], int lane) {
 #pragma unroll

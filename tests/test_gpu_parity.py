@@ -599,6 +599,45 @@ def test_real_v_projection(M, planar):
     assert same.mean() >= 0.99
 
 
+@pytest.mark.parametrize("opt", [0, "nofold"], ids=["realV", "complexV"])
+def test_projection_subspace_matches_oracle(opt):
+    """Setup test of the SVD factor V_D (eqs. 10-12) through the projection the device runs:
+    for any orthonormal basis V of the retained right-singular subspace, z_f^H z_g = x_f^H V V^H x_g, so the Gram matrix
+    of the dumped Z rows is basis-invariant and equals the oracle's (V_oracle V_oracle^H is the same projector iff the
+    subspaces agree, i.e. all principal angles are 0, and the device V is orthonormal).  Checked on real-V (R22) and
+    complex-V plans against the oracle's LAPACK SVD; tolerance: FP16 operands, FP32 accumulation."""
+    from workloads import geometry as G
+    from workloads import scenes as SC
+    rng = np.random.default_rng(4242)
+    M, N, hop, F = 6, 256, 128, 96
+    mics = rng.uniform(-0.06, 0.06, (M, 3))
+    pts = G.icosphere(2)
+    L = (F - 1) * hop + N
+    u = pts[rng.integers(len(pts))]
+    audio = SC.plane_wave_stream(rng, mics, 16000.0, 343.0, L, u, 0.0).astype(np.float32)
+    plan = S.Plan(mics, pts, 16000.0, 343.0, N, hop, "far", methods=("svd",), max_frames=F,
+                  options=0 if opt == 0 else S.OPT_NO_SVD_FOLD)
+    info = plan.info()
+    _run(plan, type("W", (), {"channel_stride": L, "frame_stride": hop})(), "svd", torch.from_numpy(audio).to(DEV), F)
+    Zd = plan.debug_dump(S.DUMP_Z, F).astype(np.float64)
+    plan.close()
+    D = info["D"]
+    Zg = (Zd[:, :D] + 1j * Zd[:, D:]) / np.sqrt(info["PK"])
+    tau = srp.tdoa(mics, pts, 16000.0, 343.0, "far")
+    fac = svd.svd_factors(tau, N, 1e-5)
+    assert fac["D"] == D
+    V = fac["V"]
+    assert np.abs(V.conj().T @ V - np.eye(D)).max() < 1e-10          # the oracle's own V is orthonormal
+    x = srp.frames_to_x(srp.extract_frames(audio, F, M, N, L, hop))
+    Zo = svd.project(V, x)
+    Gg, Go = Zg.conj() @ Zg.T, Zo.conj() @ Zo.T
+    scale = np.sqrt(np.outer(np.real(np.diag(Go)), np.real(np.diag(Go))))
+    assert np.abs(Gg - Go).max() / scale.max() < 2e-3, np.abs(Gg - Go).max() / scale.max()
+    # a subspace mistake of one dimension would move the projected energy by ~1/D of the residual: compare it too
+    eg, eo = np.real(np.diag(Gg)), np.real(np.diag(Go))
+    assert np.abs(eg - eo).max() / eo.max() < 2e-3
+
+
 def test_srp_last_fold_row():
     """The folded W of a 2562-point grid (no twins) has 1281 rows = 5 x 256 + 1: the last fold row sits alone in the
     6th 256-row tile of the CTA-pair GEMM (rows past it are zero padding).  Sources placed exactly on that row's two

@@ -19,3 +19,6 @@ echo "exit $?" >> gpurun_out/s_ncu_gemm.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"das_fold_kernel" -s 1 -c 1 -f \
     -o gpurun_out/s_prof_das4 python tools/ncu_target.py 4 srp > gpurun_out/s_ncu_das.log 2>&1
 echo "exit $?" >> gpurun_out/s_ncu_das.log
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"stft|gemm2p|gemm_kernel|zsplit|rescore|finalize" \
+    -s 6 -c 6 -f -o gpurun_out/s_prof_svd python tools/ncu_target.py 3 svd > gpurun_out/s_ncu_svd.log 2>&1
+echo "exit $?" >> gpurun_out/s_ncu_svd.log
