@@ -966,17 +966,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
 // (gemm2f_kernel, 256-column tiles, produced it once per V tile and was producer-bound at N = 160), and each V slab
 // is staged once.  One accumulator (<= 512 columns): the epilogue is not overlapped with the next tile's MMAs.
 // Warps: 0 TMA (+TMEM alloc), 1 MMA (leader), 2-5 epilogue (lane groups 2,3,0,1), 6-7 producers of the Re rows,
-// 8-9 producers of the Im rows.  Work units in unit_of_f order (split slowest, V tile, frame tile fastest).
+// 8-9 producers of the Im rows (one instruction stream for both, produce_x_part).  Work units in unit_of_f order (split slowest, V tile, frame tile fastest).
 // ================================================================================================================
 constexpr int P_A_BYTES = 128 * BK * 2;                // 16 KB: this CTA's 128 A rows (64 frames x {Re, Im})
 constexpr int P_MAX_STAGES = 8;
 
-// Producer warps of gemm2p_kernel: this thread's A row (PART 0: Re x, PART 1: Im x of frame f, eqs. 3, 7) for the bin
+// Producer warps of gemm2p_kernel: this thread's A row (part 0: Re x, part 1: Im x of frame f, eqs. 3, 7) for the bin
 // chunks [w.c0, w.c1), one 16-unit slab per stage (the last slab of a chunk holds kU % 16 units when that is 8).
-template <int Mi, int BPC, int PART, int STG>
+// `part` is a run-time (warp-uniform) value so that the Re and the Im producer warps run ONE copy of the unrolled
+// chunk body: with a copy per part the producers' code was 44 KB, past the 32 KB L1.5 instruction cache, and half of
+// their stall samples were instruction fetches (ncu r02: no_instruction on every 128-byte line, tensor pipe 40%).
+// Both parts are x = av . (r_b, i_b) with the first microphone's record viewed as av = (r_a, i_a) for Re x and
+// (i_a, -r_a) for Im x; the pairs are enumerated a-major, so av is rebuilt once per run of pairs (a, *).
+template <int Mi, int BPC, int STG>
 __device__ __forceinline__ void produce_x_part(const GemmParams& p, const Unit& w, int f, bool valid, uint8_t* smem,
                                                uint64_t* full, uint64_t* empty, int& stage, uint32_t& phase,
-                                               uint32_t row_off, uint32_t xr) {
+                                               uint32_t row_off, uint32_t xr, const bool part) {
     constexpr PairTab<Mi> PT{};
     constexpr int kPairs = Mi * (Mi - 1) / 2;
     constexpr int kUnitsRaw = (BPC == 4) ? kPairs : (kPairs + 1) / 2;
@@ -1021,6 +1026,8 @@ __device__ __forceinline__ void produce_x_part(const GemmParams& p, const Unit& 
                 asm volatile("prefetch.global.L2 [%0];" ::"l"(nxt + (int64_t)m * p.F_pad * kUB));
         }
         uint32_t pend0 = 0u, pend1 = 0u;
+        uint32_t av[BPC] = {};                 // the a-side view of the current run of pairs (a, *)
+        const uint32_t neg = part ? 0x80008000u : 0u;
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             if ((u & 15) == 0) mbar_wait(&empty[stage], phase ^ 1);
@@ -1029,13 +1036,14 @@ __device__ __forceinline__ void produce_x_part(const GemmParams& p, const Unit& 
             if constexpr (BPC == 4) {
                 if (u < kPairs) {
                     const int a = PT.i[u], b = PT.j[u];
-                    if (PART == 0) {           // Re x = ra rb + ia ib   (eq. 3)
-                        w0 = h2fma(e[a][0], e[b][0], h2mul(e[a][2], e[b][2]));
-                        w1 = h2fma(e[a][1], e[b][1], h2mul(e[a][3], e[b][3]));
-                    } else {                   // Im x = ia rb - ra ib
-                        w0 = h2fma(e[a][2], e[b][0], h2mul(e[a][0] ^ 0x80008000u, e[b][2]));
-                        w1 = h2fma(e[a][3], e[b][1], h2mul(e[a][1] ^ 0x80008000u, e[b][3]));
+                    if (b == a + 1) {          // Re x = ra rb + ia ib, Im x = ia rb - ra ib   (eq. 3)
+                        av[0] = part ? e[a][2] : e[a][0];
+                        av[1] = part ? e[a][3] : e[a][1];
+                        av[2] = (part ? e[a][0] : e[a][2]) ^ neg;
+                        av[3] = (part ? e[a][1] : e[a][3]) ^ neg;
                     }
+                    w0 = h2fma(av[0], e[b][0], h2mul(av[2], e[b][2]));
+                    w1 = h2fma(av[1], e[b][1], h2mul(av[3], e[b][3]));
                 }
             } else {
 #pragma unroll
@@ -1044,8 +1052,11 @@ __device__ __forceinline__ void produce_x_part(const GemmParams& p, const Unit& 
                     uint32_t v = 0u;
                     if (pp < kPairs) {
                         const int a = PT.i[pp], b = PT.j[pp];
-                        v = PART == 0 ? h2fma(e[a][0], e[b][0], h2mul(e[a][1], e[b][1]))
-                                      : h2fma(e[a][1], e[b][0], h2mul(e[a][0] ^ 0x80008000u, e[b][1]));
+                        if (b == a + 1) {
+                            av[0] = part ? e[a][1] : e[a][0];
+                            av[1] = (part ? e[a][0] : e[a][1]) ^ neg;
+                        }
+                        v = h2fma(av[0], e[b][0], h2mul(av[1], e[b][1]));
                     }
                     if (h == 0) w0 = v; else w1 = v;
                 }
@@ -1221,10 +1232,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
         for (int t = pair; t < units; t += n_pairs) {
             const Unit w = unit_of_f(p, t);
             const int f = w.m * 128 + (int)rank * 64 + (tp & 63);
-            if (tp < 64)
-                produce_x_part<Mi, BPC, 0, STG>(p, w, f, f < p.F, smem, full, empty, stage, phase, row_off, xr);
-            else
-                produce_x_part<Mi, BPC, 1, STG>(p, w, f, f < p.F, smem, full, empty, stage, phase, row_off, xr);
+            produce_x_part<Mi, BPC, STG>(p, w, f, f < p.F, smem, full, empty, stage, phase, row_off, xr, tp >= 64);
         }
     }
 

@@ -13,7 +13,7 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
     python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/s_ncu_bench.log 2>&1
 echo "exit $?" >> gpurun_out/s_ncu_bench.log
 python tools/ncu_target.py 3 both > gpurun_out/s_ncu_plain.log 2>&1 && \
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gemm2_kernel" -s 2 -c 1 -f \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gemm2_kernel" -s 1 -c 1 -f \
     -o gpurun_out/s_prof_srpgemm python tools/ncu_target.py 3 both > gpurun_out/s_ncu_gemm.log 2>&1
 echo "exit $?" >> gpurun_out/s_ncu_gemm.log
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"das_fold_kernel" -s 1 -c 1 -f \
