@@ -61,25 +61,37 @@ class ClockSampler:
         self.reasons: set[str] = set()
         self.sm_max = None
         self.src = "nvml"
+        self._nv = None
         self._stop = threading.Event()
         self._t = threading.Thread(target=self._run, daemon=True)
 
-    def _run_nvml(self):
-        import pynvml as nv
-        nv.nvmlInit()
+    def _nvml_open(self) -> bool:
+        """NVML is initialised here, on the caller's thread, BEFORE the timed region (inside the sampling thread the
+        import + nvmlInit took longer than a 0.1 s region when the process is pinned to few cores: 0 samples)."""
         try:
-            h = nv.nvmlDeviceGetHandleByIndex(self.dev)
-            self.sm_max = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
-            bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
-                    nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
-            while not self._stop.is_set():
-                self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
-                self.power.append(nv.nvmlDeviceGetPowerUsage(h) / 1e3)
-                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
-                self.reasons.update(n for n, b in zip(self.NAMES, bits) if r & b)
-                self._stop.wait(self.period)
-        finally:
-            nv.nvmlShutdown()
+            import pynvml as nv
+            nv.nvmlInit()
+            self._nv = nv
+            self._h = nv.nvmlDeviceGetHandleByIndex(self.dev)
+            self.sm_max = float(nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM))
+            self._bits = (nv.nvmlClocksEventReasonHwSlowdown, nv.nvmlClocksEventReasonHwThermalSlowdown,
+                          nv.nvmlClocksEventReasonSwThermalSlowdown, nv.nvmlClocksEventReasonSwPowerCap)
+            return True
+        except Exception:
+            self._nv = None
+            return False
+
+    def _sample_nvml(self):
+        nv, h = self._nv, self._h
+        self.sm.append(float(nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)))
+        self.power.append(nv.nvmlDeviceGetPowerUsage(h) / 1e3)
+        r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+        self.reasons.update(n for n, b in zip(self.NAMES, self._bits) if r & b)
+
+    def _run_nvml(self):
+        while not self._stop.is_set():
+            self._sample_nvml()
+            self._stop.wait(self.period)
 
     def _run_smi(self):
         self.src = "nvidia-smi"
@@ -100,18 +112,29 @@ class ClockSampler:
             self._stop.wait(0.2)
 
     def _run(self):
-        try:
-            self._run_nvml()
-        except Exception:
-            self._run_smi()
+        if self._nv is not None:
+            try:
+                self._run_nvml()
+                return
+            except Exception:
+                pass
+        self._run_smi()
 
     def __enter__(self):
+        self._nvml_open()
         self._t.start()
         return self
 
     def __exit__(self, *a):
         self._stop.set()
         self._t.join(timeout=10)
+        if self._nv is not None:
+            try:
+                if not self.sm:
+                    self._sample_nvml()       # never leave the line without a reading
+                self._nv.nvmlShutdown()
+            except Exception:
+                pass
 
     def summary(self) -> dict:
         if not self.sm:
@@ -398,9 +421,9 @@ def main() -> None:
         import multiprocessing as mp
         ctx = mp.get_context("fork")
         fac_conn, child = ctx.Pipe(duplex=False)
-        fac_proc = ctx.Process(target=_factors_child, args=(a.cfg, child, all_cores[1:]), daemon=True)
+        fac_proc = ctx.Process(target=_factors_child, args=(a.cfg, child, all_cores[2:] or all_cores), daemon=True)
         fac_proc.start()
-        os.sched_setaffinity(0, all_cores[:1])
+        os.sched_setaffinity(0, all_cores[:2])     # the launch thread and the clock sampler
     import torch
 
     import paper_1811_11785_b200 as S

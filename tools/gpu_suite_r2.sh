@@ -5,6 +5,7 @@
 export PYTHONPATH=$PWD
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,power.draw --format=csv > gpurun_out/s_gpu.txt
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/s_smoke.log 2>&1; echo "exit $?" >> gpurun_out/s_smoke.log
 timeout 1500 python -m pytest tests -m gpu -q --durations=15 > gpurun_out/s_tests.log 2>&1; echo "exit $?" >> gpurun_out/s_tests.log
 timeout 900 python bench.py > gpurun_out/s_bench.jsonl 2> gpurun_out/s_bench.err
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/s_ref.jsonl 2> gpurun_out/s_ref.err
