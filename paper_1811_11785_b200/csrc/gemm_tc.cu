@@ -44,8 +44,6 @@ struct GemmParams {
     int spc;                               // slabs per chunk
     int prefetch;                          // 0 none, 1 L2 prefetch of the next chunk's phasors, 2 same evict_last
     int bn;                                // frames per tile of the CTA-pair kernel (multiple of 32, <= 256)
-    int bn_last;                           // gemm2_kernel producer modes: frames of the last frame tile (0 = bn): a
-                                           // ragged batch pays MMA columns for ceil32(F mod bn) frames, not for bn
     int c_lo, c_hi;                        // active bin-chunk range (band limit, NEXT-3); producer modes only
     const int* fold_cls;                   // folded SRP (FOLD kernels): [2][fold_rows] classes of a - b / a + b
     int fold_rows;
@@ -606,8 +604,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
     const int pair = blockIdx.x >> 1, n_pairs = gridDim.x >> 1;
     const int units = p.m_tiles * p.n_tiles * p.ksplit;   // m_tiles counts 256-row pair tiles
     const int bn = p.bn, hb = p.bn / 2;                    // frames per pair tile / per CTA
-    // the last frame tile may be narrower (p.bn_last frames at the same frame origin n * bn)
-    auto tile_bn = [&](const Unit& w) { return (p.bn_last && w.n == p.n_tiles - 1) ? p.bn_last : bn; };
+    const uint32_t idesc = umma_idesc_f16(256, (uint32_t)bn);
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < kSt; ++s) {
@@ -669,7 +666,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
             uint32_t acc_phase = 0;
             for (int t = pair; t < units; t += n_pairs) {
                 const Unit w = unit_of(p, t);
-                const uint32_t idesc = umma_idesc_f16(256, (uint32_t)tile_bn(w));
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 int lp = 0;                                         // slab pair within the bin chunk (FOLD)
@@ -727,14 +723,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
             tc_fence_after();
             const int row = w.m * 256 + (int)rank * 128 + g * 32 + lane;
             const bool row_ok = row < p.rows_valid;
-            const int bn_t = tile_bn(w);
             int cls_m = row, cls_p = -1;                            // classes scored by this accumulator row
             if (FOLD && row_ok) {
                 cls_m = p.fold_cls[row];
                 cls_p = p.fold_cls[p.fold_rows + row];
             }
 #pragma unroll 1
-            for (int j0 = 0; j0 < bn_t; j0 += 32) {
+            for (int j0 = 0; j0 < bn; j0 += 32) {
                 uint32_t r[32], rb[32];
                 tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + acc * BN + j0, r);
                 if (FOLD) tmem_ld_32x32b_x32(tmem_base + (uint32_t(g * 32) << 16) + BN + j0, rb);
@@ -790,9 +785,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS2, 1)
         uint32_t phase = 0;
         for (int t = pair; t < units; t += n_pairs) {
             const Unit w = unit_of(p, t);
-            const int hb_t = tile_bn(w) / 2;
-            const int f = w.n * bn + (int)rank * hb_t + tp;
-            const bool valid = f < p.F && tp < hb_t;
+            const int f = w.n * bn + (int)rank * hb + tp;
+            const bool valid = f < p.F && tp < hb;
             produce_x_pair<Mi, BPC, kSt, kBS, FOLD, B2_BYTES>(p, w, f, valid, sB, full, empty, stage, phase, row_off,
                                                               xr);
         }
@@ -1497,8 +1491,6 @@ cudaError_t launch_gemm(const Plan& p, const Band& b, int mode, int F, cudaStrea
     if (mode == 0 && p.pair_srp) {
         gp.bn = 256;                   // r01: 224 (the wave-quantisation optimum) was slower under the power cap
         gp.n_tiles = (F + gp.bn - 1) / gp.bn;
-        // ragged batch (cfg3: 10^4 = 39 x 256 + 16): the last frame tile runs N = 32 MMAs instead of 256
-        gp.bn_last = ((F - (gp.n_tiles - 1) * gp.bn) + 31) / 32 * 32;
         if (both && p.tail_n > 0) gp.m_tiles = p.tail_r0 / 256;   // the tail rows are scored by the projection
         // (a BOTH call reaches here only on the argmax path: srp_split_ways(p, b, F) == 1, see localize_impl)
         const int units = gp.m_tiles * gp.n_tiles;
