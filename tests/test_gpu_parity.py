@@ -599,6 +599,44 @@ def test_real_v_projection(M, planar):
     assert same.mean() >= 0.99
 
 
+@pytest.mark.parametrize("seed", [910, 911])
+def test_search_candidate_overflow(seed):
+    """FP16 search + exact rescore when the candidate lists overflow: at rank 1 the scores
+    Re{D^_q Z^} (eq. 14) of hundreds of classes lie within SEARCH_TAU = 2.5e-3 of the frame maximum, more than the 128
+    entries a list holds, so rescore_kernel falls back to the exact FP32 scores of every class.  Every returned q must
+    then be the oracle's argmax or a near-tie of it (R18), and Y_q (Alg. 1 step 4) must match at the returned q."""
+    from workloads import geometry as G
+    from workloads import scenes as SC
+    rank = 1
+    rng = np.random.default_rng(seed)
+    M, N, hop, F = 4, 256, 128, 96
+    mics = rng.uniform(-0.05, 0.05, (M, 3))
+    pts = G.icosphere(4)
+    L = (F - 1) * hop + N
+    u = pts[rng.integers(len(pts))]
+    audio = SC.plane_wave_stream(rng, mics, 16000.0, 343.0, L, u, 5.0).astype(np.float32)
+    plan = S.Plan(mics, pts, 16000.0, 343.0, N, hop, "far", rank_D=rank, methods=("svd",), max_frames=F)
+    assert plan.info()["D"] == rank
+    q, sc = _run(plan, type("W", (), {"channel_stride": L, "frame_stride": hop})(), "svd",
+                 torch.from_numpy(audio).to(DEV), F)
+    plan.close()
+    tau = srp.tdoa(mics, pts, 16000.0, 343.0, "far")
+    fac = svd.svd_factors(tau, N, rank=rank)
+    x = srp.frames_to_x(srp.extract_frames(audio, F, M, N, L, hop))
+    keep = _check_degenerate(q, sc, x)
+    S_ref, Y_at = PP.svd_reference(fac, tau, x[keep], N)
+    near = (S_ref >= S_ref.max(axis=1, keepdims=True) - 2.0e-3).sum(axis=1)
+    assert np.median(near) > 128, f"the overflow path is not exercised (median {np.median(near)} near-maximal rows)"
+    qk, sk = q[keep], sc[keep]
+    for f in range(len(qk)):
+        g = int(qk[f])
+        assert 0 <= g < len(pts)
+        best = S_ref[f].max()
+        assert best - S_ref[f, g] <= PP.TOL * abs(best), (f, g, best, S_ref[f, g])
+        y = Y_at(f, g)
+        assert abs(float(sk[f]) - y) <= PP.TOL * max(abs(y), 1.0), (f, g, sk[f], y)
+
+
 @pytest.mark.parametrize("opt", [0, "nofold"], ids=["realV", "complexV"])
 def test_projection_subspace_matches_oracle(opt):
     """Setup test of the SVD factor V_D (eqs. 10-12) through the projection the device runs:
