@@ -286,6 +286,14 @@ def _dist():
     return dist, rank, ws, local
 
 
+def workload_config(cfg: int, w, Q: int, D: int, ws: int) -> dict:
+    """`config` of the JSON line: names the workload; identical for both arms (the reference arm times a bounded
+    sample of it per step and says so in cpu_baseline.sample)."""
+    return {"workload": f"cfg{cfg}", "name": w.name, "frames_per_step": w.n_frames, "M": w.M, "N": w.N,
+            "Q": int(Q), "D": int(D), "delta": w.delta, "methods": "SRP-PHAT+SVD-PHAT",
+            "l2": "inputs larger than L2 (audio 655 MB, W 2.57 GB per step)", "parallelism": f"frames x{ws}"}
+
+
 def run_reference(a) -> None:
     """--impl reference: the oracle (the deliberately slow CPU program) on the box's host cores, same metric."""
     dist, rank, ws, local = _dist()
@@ -306,7 +314,7 @@ def run_reference(a) -> None:
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": a.gpus, "steps": a.steps,
             "warmup": a.warmup, "ms_per_step": 1e3 * sec / a.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"cfg{a.cfg}", "frames_per_step": per},
+            "config": workload_config(a.cfg, w, len(w.points), factors[1]["D"], ws), "reference_frames_per_step": per,
             "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle",
                              "sample": (f"{per} cfg{a.cfg} frames per step through the oracle's SRP-PHAT online path "
                                         "(W regenerated per step) and SVD-PHAT online path (factors computed once, "
@@ -538,9 +546,7 @@ def main() -> None:
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": a.steps, "warmup": max(3, a.warmup),
         "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f16",
         "data": "synthetic",
-        "config": {"workload": f"cfg{a.cfg}", "name": w.name, "frames_per_step": F, "M": w.M, "N": w.N,
-                   "Q": info["Q"], "D": info["D"], "delta": w.delta, "methods": "SRP-PHAT+SVD-PHAT",
-                   "l2": "inputs larger than L2 (audio 655 MB, W 2.57 GB per step)", "parallelism": f"frames x{ws}"},
+        "config": workload_config(a.cfg, w, info["Q"], info["D"], ws),
         "srp_fps": F * ws / (srp_ms / 1e3), "svd_fps": F * ws / (svd_ms / 1e3),
         "stage_ms": stage_ms, "gpu_launches": launches,
         "roofline": roof, "roofline_svd": roof_svd,
