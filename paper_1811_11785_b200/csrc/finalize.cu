@@ -331,30 +331,69 @@ __global__ void __launch_bounds__(32 * FIN_WARPS, NM == 1 ? 4 : 3)
 }
 
 // Small-batch SRP: Y[f][q] = sum of the S partial power maps (fixed order: deterministic), argmax over the steering
-// classes (lowest index on ties) -> the frame's key.  Warp per frame.
-__global__ void split_argmax_kernel(const float* __restrict__ Yp, int S, int64_t F_pad, int ldq, int Q, int F,
-                                    unsigned long long* __restrict__ keys) {
-    const int f = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int lane = threadIdx.x & 31;
+// classes (lowest index on ties) -> the frame's key.  CTA per frame, 16-byte loads, the 4 x S loads of a thread in
+// flight together (a warp per frame with scalar loads left 32 CTAs on the GPU and took 82 us for the 17 MB of a
+// 256-frame cfg5 call, ncu r02: as long as the split GEMM it follows).
+constexpr int SA_THREADS = 256;
+__global__ void __launch_bounds__(SA_THREADS)
+    split_argmax_kernel(const float* __restrict__ Yp, int S, int64_t F_pad, int ldq, int Q, int F,
+                        unsigned long long* __restrict__ keys) {
+    __shared__ unsigned long long s_best[SA_THREADS / 32];
+    const int f = blockIdx.x, t = threadIdx.x;
     if (f >= F) return;
+    const int n4 = ldq >> 2;                                 // ldq = Q_pad, a multiple of 128
     unsigned long long best = 0ull;
-    for (int q = lane; q < Q; q += 32) {
-        float v = 0.f;
-        for (int s = 0; s < S; ++s) v += Yp[((int64_t)s * F_pad + f) * ldq + q];
-        const unsigned long long k = v == v ? ((unsigned long long)f2o_dev(v) << 32) | (0xFFFFFFFFull - (uint32_t)q) : 0ull;
-        best = k > best ? k : best;
+    for (int i0 = 0; i0 < n4; i0 += 4 * SA_THREADS) {
+        float4 v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) v[j] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int sp = 0; sp < S; ++sp) {
+            const float4* row = reinterpret_cast<const float4*>(Yp + ((int64_t)sp * F_pad + f) * ldq);
+            float4 w[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int i = i0 + t + j * SA_THREADS;
+                w[j] = i < n4 ? row[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                v[j].x += w[j].x;
+                v[j].y += w[j].y;
+                v[j].z += w[j].z;
+                v[j].w += w[j].w;
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int q0 = 4 * (i0 + t + j * SA_THREADS);
+            const float e[4] = {v[j].x, v[j].y, v[j].z, v[j].w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int q = q0 + c;
+                const unsigned long long k =
+                    (q < Q && e[c] == e[c]) ? ((unsigned long long)f2o_dev(e[c]) << 32) | (0xFFFFFFFFull - (uint32_t)q)
+                                            : 0ull;
+                best = k > best ? k : best;
+            }
+        }
     }
 #pragma unroll
     for (int o = 16; o >= 1; o >>= 1) {
         const unsigned long long ob = __shfl_xor_sync(0xffffffffu, best, o);
         best = ob > best ? ob : best;
     }
-    if (lane == 0) keys[f] = best;
+    if ((t & 31) == 0) s_best[t >> 5] = best;
+    __syncthreads();
+    if (t == 0) {
+#pragma unroll
+        for (int w = 1; w < SA_THREADS / 32; ++w) best = s_best[w] > best ? s_best[w] : best;
+        keys[f] = best;
+    }
 }
 
 cudaError_t launch_split_argmax(const Plan& p, int F, int S, cudaStream_t s) {
     if (F <= 0) return cudaSuccess;
-    split_argmax_kernel<<<(F * 32 + 255) / 256, 256, 0, s>>>(p.d_Ypart, S, p.F_pad, p.Q_pad, p.Q_eff, F, p.d_keys);
+    split_argmax_kernel<<<F, SA_THREADS, 0, s>>>(p.d_Ypart, S, p.F_pad, p.Q_pad, p.Q_eff, F, p.d_keys);
     return cudaGetLastError();
 }
 
