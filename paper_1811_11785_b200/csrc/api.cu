@@ -731,16 +731,30 @@ static svdphat_status localize_impl(Plan& p, const Band& b, int32_t method, cons
     const bool das = (method & SVDPHAT_METHOD_SRP) && das_active(p, F);
     // SRP tail rows scored through the projection: BOTH calls on the argmax GEMM path (not the small-batch split)
     const bool both = method == SVDPHAT_METHOD_BOTH && !das && p.tail_n > 0 && srp_split_ways(p, b, F) == 1;
-    if (das) {
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_BINS, sr, [&] { return launch_das_bins(p, b, F, sr); }));
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_DAS, sr, [&] { return launch_das(p, b, F, sr); }));
-    } else if (method & SVDPHAT_METHOD_SRP) {
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_GEMM, sr, [&] { return launch_gemm(p, b, 0, F, sr, both); }));
-    }
-    if (method & SVDPHAT_METHOD_SVD) {
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_PROJ, sv, [&] { return launch_gemm(p, b, 1, F, sv); }));
-        SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_NORM, sv, [&] { return launch_zsplit(p, b, F, sv, both); }));
-    }
+    auto run_srp = [&]() -> svdphat_status {
+        if (das) {
+            SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_BINS, sr, [&] { return launch_das_bins(p, b, F, sr); }));
+            SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_DAS, sr, [&] { return launch_das(p, b, F, sr); }));
+        } else if (method & SVDPHAT_METHOD_SRP) {
+            SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SRP_GEMM, sr, [&] { return launch_gemm(p, b, 0, F, sr, both); }));
+        }
+        return SVDPHAT_OK;
+    };
+    auto run_proj = [&]() -> svdphat_status {
+        if (method & SVDPHAT_METHOD_SVD) {
+            SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_PROJ, sv, [&] { return launch_gemm(p, b, 1, F, sv); }));
+            SVD_CUDA_TRY(staged(p, SVDPHAT_STAGE_SVD_NORM, sv, [&] { return launch_zsplit(p, b, F, sv, both); }));
+        }
+        return SVDPHAT_OK;
+    };
+    // Small batches (the split-K SRP path, cfg5's 256-frame calls): both GEMMs want whole SMs and neither fills the GPU
+    // for long, so the short projection (26 us at cfg5) goes first and the rest of the SVD chain runs beside the SRP
+    // GEMM (102 us); SRP first left the whole SVD chain (84 us) behind it (ncu r02).  Large batches: SRP first (r01 A/B).
+    const bool svd_first = fork && !das && (method & SVDPHAT_METHOD_SRP) && srp_split_ways(p, b, F) > 1;
+    svdphat_status st_l = svd_first ? run_proj() : run_srp();
+    if (st_l != SVDPHAT_OK) return st_l;
+    st_l = svd_first ? run_srp() : run_proj();
+    if (st_l != SVDPHAT_OK) return st_l;
     // forked: the SRP half of the finalize runs on the SRP stream while the SVD search is still busy (after zsplit
     // when the SRP tail rows' keys come from it)
     if (fork && (method & SVDPHAT_METHOD_SRP)) {
