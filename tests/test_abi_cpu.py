@@ -167,3 +167,31 @@ def test_bench_aggregation_two_ranks():
     for _, ms, v in res:
         assert ms == 20.0                       # max over ranks
         assert v == pytest.approx(2000 / 0.020)  # all ranks' frames / max time
+
+
+def test_bench_arms_share_the_workload_config():
+    """Both bench arms print the same `config` (the reference arm times a bounded sample of that workload)."""
+    import bench
+    from workloads import make
+    w = make(1)
+    a = bench.workload_config(1, w, len(w.points), 39, 1)
+    b = bench.workload_config(1, w, len(w.points), 39, 1)
+    assert a == b and a["workload"] == "cfg1" and a["frames_per_step"] == w.n_frames
+    assert "model" not in a
+
+
+def test_committed_launch_list_parses_and_names_the_dominant_kernel():
+    """profiles/r02/final: the ncu launch list of the bench command summarises to per-step shares in which the SRP
+    GEMM is the dominant kernel (the kernel bench.py's `roofline` object describes)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    csv_path = os.path.join(root, "profiles", "r02", "final", "ncu_launches_bench.csv")
+    if not os.path.exists(csv_path):
+        pytest.skip("no committed launch list")
+    out = subprocess.run([sys.executable, os.path.join(root, "tools", "launch_summary.py"), csv_path],
+                         capture_output=True, text=True, check=True).stdout
+    step = out[out.index("per localize(BOTH) step"):]
+    first = [ln for ln in step.splitlines()[1:] if ln.startswith("svdphat::")][0]
+    assert "gemm2_kernel" in first and float(first.split()[-1].rstrip("%")) > 70.0
